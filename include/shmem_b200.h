@@ -1,0 +1,120 @@
+/*
+ * shmem_b200.h — C ABI of the B200-native fused AllGather+GEMM / GEMM+ReduceScatter
+ * path (symmetric heap over NVLink + sm_100a tcgen05 kernels).
+ *
+ * This is the drop-in boundary for the reference package `minishmem`
+ * (/root/reference/pkg/src/minishmem).  Every entry point below replaces one
+ * reference interface; the Python mirror in paper_2504_19442_b200/ binds
+ * these with ctypes exactly as a maintainer would from the reference side
+ * (see INTEGRATION.md).
+ *
+ * Conventions
+ *   - every function returns int status: SH_OK (0) or one of SH_ERR_*; the
+ *     message of the last failure on the calling thread is sh_last_error().
+ *   - pointers are device pointers on the rank's GPU unless stated; sizes in
+ *     bytes; matrices are row-major, dtype bf16 (SH_DTYPE_BF16) or fp16.
+ *   - `stream` is a cudaStream_t (may be NULL = legacy default stream); all
+ *     device work is enqueued on it (stream-ordered, asynchronous).
+ *   - signals are u64 words in a pad at the tail of each rank's slab; a
+ *     signal index `sig` addresses slab + heap_bytes + 8*sig on every rank
+ *     (reference core.py:242-261).
+ */
+#ifndef SHMEM_B200_H
+#define SHMEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SH_OK 0
+#define SH_ERR_ARG 1     /* maps to ArgumentError       (reference errors.py:19)  */
+#define SH_ERR_ALLOC 2   /* maps to AllocationError     (reference errors.py:15)  */
+#define SH_ERR_TIMEOUT 3 /* maps to SynchronizationFault (reference errors.py:27) */
+#define SH_ERR_CUDA 4    /* CUDA runtime/driver failure                           */
+#define SH_ERR_STATE 5   /* maps to UsageError          (reference errors.py:31)  */
+#define SH_ERR_CONFIG 6  /* maps to ConfigurationError  (reference errors.py:11)  */
+
+#define SH_DTYPE_BF16 0
+#define SH_DTYPE_FP16 1
+
+#define SH_MAX_WORLD 16
+
+typedef struct sh_world sh_world;
+
+/* Library identity / diagnostics. */
+int sh_version(void);
+const char* sh_last_error(void);
+
+/* World bring-up: replaces WorldSpec/World.__init__/init_world
+ * (reference core.py:35-66, 151-187, 565-567).
+ * Single-process world: rank r lives on devices[r] (ranks may share a GPU);
+ * every slab is mapped into every rank (peer access over NVLink). */
+int sh_world_create(int world_size, const int* devices, size_t heap_bytes, int signal_count,
+                    double timeout_s, sh_world** out);
+/* One process per GPU (torchrun): allocate this rank's slab; peers are
+ * attached with sh_import_ipc_handles after an out-of-band all-gather. */
+int sh_world_create_member(int world_size, int rank, int device, size_t heap_bytes,
+                           int signal_count, double timeout_s, sh_world** out);
+int sh_ipc_handle_size(void);
+int sh_export_ipc_handle(sh_world* w, void* handle_out);
+int sh_import_ipc_handles(sh_world* w, const void* handles /* world_size * handle_size */);
+int sh_world_destroy(sh_world* w);
+
+/* Symmetric allocation: replaces World.alloc_symmetric / alloc_signals
+ * (reference core.py:211-237).  Same offset / base on every rank. */
+int sh_alloc(sh_world* w, size_t nbytes, size_t align, size_t* offset);
+int sh_alloc_signals(sh_world* w, int count, int* base);
+
+/* Address resolution: replaces World._abs / _sig_abs (reference core.py:254-261).
+ * Pointer to `peer`'s replica as seen from `rank`'s device. */
+int sh_heap_ptr(sh_world* w, int rank, int peer, size_t offset, void** ptr);
+int sh_signal_ptr(sh_world* w, int rank, int peer, int sig, void** ptr);
+
+/* Signal maintenance: replaces sig_read / _reset_own_signals / tuning.reset_signals
+ * (reference core.py:263-301, collectives.py:67-69, tuning.py:79-91). */
+int sh_read_signals(sh_world* w, int rank, int base, int count, uint64_t* out_host);
+int sh_reset_signals(sh_world* w, int rank, int base, int count, void* stream);
+
+/* Device-side timeouts (bounded spins) land in a host-mapped error word per
+ * rank; nonzero => SynchronizationFault (reference sched.py:227-238). */
+int sh_poll_error(sh_world* w, int rank, int* code);
+int sh_clear_error(sh_world* w, int rank);
+
+/* Fused AllGather+GEMM for rank `rank`: replaces pipelines.ag_gemm
+ * (reference pipelines.py:97-150) including its comm half
+ * allgather_push_intra(wait_all=False) (collectives.py:83-102).
+ *   a_shard : (m/W, k) this rank's rows        b : (k, n)        c : (m, n) out
+ *   gathered_off : offset of the symmetric (W*m/W*k) gather buffer
+ *   ready_base   : W signals; ready[src] = epoch once src's shard landed here
+ *   done_base    : W signals; done[p] = epoch once rank p finished the call
+ *   chunk_order  : W ints, a permutation (first-visit order of the TileSchedule)
+ *   epoch        : monotone call counter (>= 1), identical on every rank */
+int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* c,
+               size_t gathered_off, int ready_base, int done_base, int m, int n, int k, int dtype,
+               const int* chunk_order, uint64_t epoch, void* stream);
+
+/* Fused GEMM+ReduceScatter for rank `rank`: replaces pipelines.gemm_rs
+ * (reference pipelines.py:179-216) with rs_intra_streams (collectives.py:131-175).
+ *   a : (m, k)   b : (k, n)   out : (m/W, n) = row block `rank` of sum_r a_r @ b_r
+ *   staging_off   : offset of the symmetric W*(m/W)*n staging buffer
+ *   producer_base : W signals; producer[d] = epoch once rank d reduced this call
+ *   reduction_base: W signals; reduction[s] counts elements delivered by s */
+int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
+               size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
+               int dtype, const int* chunk_order, uint64_t epoch, void* stream);
+
+/* The GEMM core alone (TP=1, no symmetric heap): c(m,n) = a(m,k) @ b(k,n). */
+int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream);
+
+/* Tile override for tuning: bn in {0 (auto), 128, 256}; cta_group in {0 (auto), 1, 2}. */
+int sh_set_tile_config(int bn, int cta_group);
+/* Launch config chosen for a problem (for the bench's roofline bookkeeping). */
+int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHMEM_B200_H */

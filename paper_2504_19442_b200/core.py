@@ -1,0 +1,627 @@
+"""World construction and the GPU symmetric heap (hot-path subsystem 1).
+
+Same geometry and addressing as the reference (pkg/src/minishmem/core.py):
+every rank owns a slab of ``heap_bytes + 8*signal_count`` bytes, a symmetric
+handle is an (offset, length) valid in every slab, and signal ``sig`` is the
+u64 at ``slab + heap_bytes + 8*sig`` (core.py:159-160, 242-261).  The slabs
+are device memory: in one process every rank's slab is peer-mapped into every
+other rank's GPU (NVLink / NVSwitch); across processes (torchrun, one rank per
+GPU) the slabs are exchanged with CUDA IPC handles.  All of it lives in the C
+ABI (``_lib``); this module is the Python mirror of the reference's World.
+
+Two ways to build a world:
+
+* ``init_world(WorldSpec(world_size=W))`` -- the reference's model: all ranks
+  are threads of this process, ``world.run(fn)`` calls ``fn(pe)`` once per rank
+  concurrently and returns the per-rank results (core.py:449-487).  Rank r uses
+  GPU ``devices[r]`` (default ``r % torch.cuda.device_count()``), so W ranks may
+  share one GPU (each rank gets its own CUDA stream).
+* ``init_world_dist(...)`` -- one process per GPU under torch.distributed;
+  ``run(fn)`` executes this process's rank only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from collections import deque
+from dataclasses import dataclass
+
+from . import _lib
+from .errors import (
+    ArgumentError,
+    CollectiveFault,
+    ConfigurationError,
+    RangeError,
+    SynchronizationFault,
+)
+
+SIG_BYTES = 8
+
+
+@dataclass(frozen=True)
+class WorldSpec:
+    """Rank geometry plus per-rank slab sizing (reference core.py:35-66).
+
+    ``devices`` (B200 extension) pins rank r to GPU ``devices[r]``."""
+
+    world_size: int
+    n_nodes: int = 1
+    local_world_size: int | None = None
+    heap_bytes: int = 1 << 20
+    signal_count: int | None = None
+    timeout_s: float = 5.0
+    devices: tuple | None = None
+
+    def __post_init__(self):
+        lws = self.local_world_size
+        if lws is None:
+            if self.n_nodes < 1 or self.world_size % self.n_nodes:
+                raise ConfigurationError(
+                    f"world_size {self.world_size} not divisible by n_nodes {self.n_nodes}")
+            lws = self.world_size // self.n_nodes
+            object.__setattr__(self, "local_world_size", lws)
+        if self.world_size < 1 or self.n_nodes < 1 or lws < 1:
+            raise ConfigurationError("world_size, n_nodes, local_world_size must be >= 1")
+        if self.world_size != self.n_nodes * lws:
+            raise ConfigurationError(
+                f"world_size {self.world_size} != n_nodes {self.n_nodes} x local {lws}")
+        if self.heap_bytes <= 0:
+            raise ConfigurationError("heap_bytes must be > 0")
+        if self.signal_count is None:
+            object.__setattr__(self, "signal_count", max(4 * self.world_size, 64))
+        if self.signal_count < self.world_size:
+            raise ConfigurationError("signal_count must be >= world_size")
+        if self.timeout_s <= 0:
+            raise ConfigurationError("timeout_s must be > 0")
+        if self.devices is not None:
+            devs = tuple(int(d) for d in self.devices)
+            if len(devs) != self.world_size:
+                raise ConfigurationError("devices must name one GPU per rank")
+            object.__setattr__(self, "devices", devs)
+
+
+@dataclass(frozen=True)
+class RankCtx:
+    rank: int
+    node_id: int
+    local_rank: int
+
+
+@dataclass(frozen=True)
+class SymHandle:
+    """Rank-independent (offset, length) into every rank's slab."""
+
+    offset: int
+    length: int
+
+    def check(self, off, nbytes):
+        if off < 0 or nbytes < 0 or off + nbytes > self.length:
+            raise RangeError(f"access [{off}, {off + nbytes}) outside handle of {self.length} bytes")
+
+
+@dataclass(frozen=True)
+class SignalSet:
+    """Contiguous signal words in the symmetric pad."""
+
+    base: int
+    count: int
+
+    def at(self, i):
+        if i < 0 or i >= self.count:
+            raise ArgumentError(f"signal index {i} out of {self.count}")
+        return self.base + i
+
+
+class Pe:
+    """A rank bound to its world, GPU and stream (reference primitives.py:76-96)."""
+
+    def __init__(self, world, ctx: RankCtx, device: int):
+        self.world = world
+        self.ctx = ctx
+        self.rank = ctx.rank
+        self.device = device
+        self._stream = None
+
+    @property
+    def torch_device(self):
+        import torch
+
+        return torch.device("cuda", self.device)
+
+    def stream(self):
+        """This rank's CUDA stream (one per rank, so ranks sharing a GPU run
+        concurrently)."""
+        import torch
+
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(device=self.device)
+        return self._stream
+
+    def barrier_all(self):
+        """Host-side rendezvous of every rank (plus device drain)."""
+        self.world._barrier(self)
+
+    def __repr__(self):
+        return f"Pe(rank={self.rank}, device=cuda:{self.device})"
+
+
+class _HostBarrier:
+    def __init__(self, parties):
+        self.parties = parties
+        self.cond = threading.Condition()
+        self.count = 0
+        self.phase = 0
+
+    def wait(self, timeout):
+        with self.cond:
+            phase = self.phase
+            self.count += 1
+            if self.count == self.parties:
+                self.count = 0
+                self.phase += 1
+                self.cond.notify_all()
+                return
+            if not self.cond.wait_for(lambda: self.phase != phase, timeout=timeout):
+                raise SynchronizationFault("barrier_all timed out")
+
+
+def _check_stream_queues(devs):
+    """Ranks sharing a GPU each use a compute and a copy stream; every one of
+    them needs its own hardware queue, or a spinning kernel can block the
+    copy it waits for (false dependency).  CUDA_DEVICE_MAX_CONNECTIONS is read
+    at context creation, so refuse loudly instead of deadlocking."""
+    import os
+    from collections import Counter
+
+    per_dev = max(Counter(devs).values())
+    if per_dev <= 1:
+        return
+    need = 2 * per_dev + 2
+    have = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
+    if have < need:
+        raise ConfigurationError(
+            f"{per_dev} ranks share one GPU: set CUDA_DEVICE_MAX_CONNECTIONS>={need} before "
+            "CUDA initialises (import paper_2504_19442_b200 before torch does it)")
+
+
+class World:
+    """Symmetric heap + signal pads on GPUs, per-rank execution contexts."""
+
+    def __init__(self, spec: WorldSpec, scheduler="free", seed=0, *, _member=None):
+        import torch
+
+        if spec.n_nodes != 1:
+            raise ConfigurationError("multi-node worlds are out of scope for the GPU path "
+                                     "(one NVSwitch node); use n_nodes=1")
+        if scheduler not in ("free", None):
+            # the reference's cooperative schedulers fuzz CPU thread
+            # interleavings; GPU concurrency is real hardware
+            raise ConfigurationError(f"scheduler {scheduler!r} is CPU-only; the GPU world is 'free'")
+        if not torch.cuda.is_available():
+            raise ConfigurationError("no CUDA device: the symmetric heap lives in GPU memory")
+        self.spec = spec
+        self._lib = _lib.load()
+        self._handle = ctypes.c_void_p()
+        self._closed = False
+        self._counters = [dict() for _ in range(spec.world_size)]
+        self._stats_lock = threading.Lock()
+        self._reset_sets = set()
+        self._reset_lock = threading.Lock()
+        self._epoch_holders = []
+        lws = spec.local_world_size
+        self.ranks = [RankCtx(r, r // lws, r % lws) for r in range(spec.world_size)]
+        ndev = torch.cuda.device_count()
+        if _member is None:
+            devs = spec.devices or tuple(r % ndev for r in range(spec.world_size))
+            _check_stream_queues(devs)
+            arr = _lib.int_array(devs)
+            _lib.check(self._lib.sh_world_create(spec.world_size, arr, spec.heap_bytes,
+                                                 spec.signal_count, float(spec.timeout_s),
+                                                 ctypes.byref(self._handle)))
+            self.local_ranks = list(range(spec.world_size))
+            self.devices = list(devs)
+        else:
+            rank, device = _member
+            _lib.check(self._lib.sh_world_create_member(
+                spec.world_size, rank, device, spec.heap_bytes, spec.signal_count,
+                float(spec.timeout_s), ctypes.byref(self._handle)))
+            self.local_ranks = [rank]
+            self.devices = [device if r == rank else -1 for r in range(spec.world_size)]
+        self.pes = [Pe(self, ctx, self.devices[ctx.rank]) if ctx.rank in self.local_ranks else None
+                    for ctx in self.ranks]
+        self._barrier_obj = _HostBarrier(len(self.local_ranks))
+        self._workers = None
+        self._dist = _member is not None
+
+    # ------------------------------------------------------------------
+    # geometry
+
+    @property
+    def world_size(self):
+        return self.spec.world_size
+
+    @property
+    def n_nodes(self):
+        return self.spec.n_nodes
+
+    @property
+    def local_world_size(self):
+        return self.spec.local_world_size
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def pe(self, rank):
+        p = self.pes[rank]
+        if p is None:
+            raise ArgumentError(f"rank {rank} is not hosted by this process")
+        return p
+
+    # ------------------------------------------------------------------
+    # symmetric allocation (reference core.py:211-237)
+
+    def alloc_symmetric(self, nbytes, align=8):
+        if nbytes < 0:
+            raise ArgumentError("negative allocation")
+        off = ctypes.c_size_t()
+        _lib.check(self._lib.sh_alloc(self._handle, nbytes, align, ctypes.byref(off)))
+        return SymHandle(off.value, nbytes)
+
+    def alloc_signals(self, count):
+        if count < 0:
+            raise ArgumentError("negative signal allocation")
+        base = ctypes.c_int()
+        _lib.check(self._lib.sh_alloc_signals(self._handle, count, ctypes.byref(base)))
+        return SignalSet(base.value, count)
+
+    # ------------------------------------------------------------------
+    # addresses and raw access
+
+    def heap_ptr(self, rank, handle: SymHandle, off=0, peer=None):
+        """Device address of ``peer``'s replica of ``handle`` as seen from
+        ``rank``'s GPU (peer defaults to rank)."""
+        handle.check(off, 0)
+        ptr = ctypes.c_void_p()
+        _lib.check(self._lib.sh_heap_ptr(self._handle, rank, rank if peer is None else peer,
+                                         handle.offset + off, ctypes.byref(ptr)))
+        return ptr.value
+
+    def _local_rank_for(self, rank):
+        if rank in self.local_ranks:
+            return rank
+        return self.local_ranks[0]
+
+    def heap_view(self, rank, handle: SymHandle, dtype, shape, off=0, peer=None):
+        """Zero-copy CUDA tensor view of ``peer``'s replica of ``handle`` as
+        mapped on ``rank``'s GPU (reference core.py:245-252)."""
+        import math
+
+        import torch
+
+        nbytes = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
+        handle.check(off, nbytes)
+        ptr = self.heap_ptr(rank, handle, off, peer=peer)
+        typestr = {torch.uint8: "|u1", torch.bfloat16: "<V2", torch.float16: "<f2",
+                   torch.int64: "<i8", torch.float32: "<f4"}[dtype]
+
+        class _Arr:
+            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                        "data": (ptr, False), "version": 2}
+
+        if dtype == torch.bfloat16:
+            # no bf16 typestr in the interface: view as int16 and reinterpret
+            _Arr.__cuda_array_interface__["typestr"] = "<i2"
+            return torch.as_tensor(_Arr(), device=torch.device("cuda", self.devices[rank])).view(
+                torch.bfloat16)
+        return torch.as_tensor(_Arr(), device=torch.device("cuda", self.devices[rank]))
+
+    def read_tensor(self, rank, handle: SymHandle, dtype, shape, off=0):
+        """Device-side copy of rank's replica of ``handle`` (for layout checks
+        of the gathered / staging buffers)."""
+        import torch
+
+        viewer = self._local_rank_for(rank)
+        torch.cuda.synchronize(self.devices[viewer])
+        view = self.heap_view(viewer, handle, dtype, shape, off, peer=rank)
+        out = view.clone()
+        torch.cuda.synchronize(self.devices[viewer])
+        return out
+
+    def read_from(self, rank, handle: SymHandle, off, nbytes):
+        """Bytes of rank's replica (reference core.py:326-328)."""
+        import torch
+
+        handle.check(off, nbytes)
+        t = self.read_tensor(rank, handle, torch.uint8, (nbytes,), off)
+        return bytes(t.cpu().numpy().tobytes())
+
+    def _dev_of(self, rank):
+        d = self.devices[rank]
+        return d if d >= 0 else self.devices[self.local_ranks[0]]
+
+    def sig_read(self, rank, sig):
+        out = (ctypes.c_uint64 * 1)()
+        _lib.check(self._lib.sh_read_signals(self._handle, rank, sig, 1, out))
+        return int(out[0])
+
+    def read_signals(self, rank, sigs: SignalSet):
+        out = (ctypes.c_uint64 * max(1, sigs.count))()
+        _lib.check(self._lib.sh_read_signals(self._handle, rank, sigs.base, sigs.count, out))
+        return [int(out[i]) for i in range(sigs.count)]
+
+    def zero_signals(self, rank, base, count, stream=None):
+        _lib.check(self._lib.sh_reset_signals(self._handle, rank, base, count,
+                                              ctypes.c_void_p(stream or 0)))
+
+    def zero_all_signals(self):
+        import torch
+
+        for r in self.local_ranks:
+            torch.cuda.synchronize(self._dev_of(r))
+            self.zero_signals(r, 0, self.spec.signal_count)
+            torch.cuda.synchronize(self._dev_of(r))
+        for holder in self._epoch_holders:
+            holder.reset_epochs()
+
+    def sweep_signals(self):
+        """{(rank, sig): value} for every nonzero signal word of local ranks."""
+        hot = {}
+        for r in self.local_ranks:
+            vals = self.read_signals(r, SignalSet(0, self.spec.signal_count))
+            for s, v in enumerate(vals):
+                if v:
+                    hot[(r, s)] = v
+        return hot
+
+    # ------------------------------------------------------------------
+    # instrumentation (reference core.py:420-432)
+
+    def bump(self, rank, name, n=1):
+        with self._stats_lock:
+            c = self._counters[rank]
+            c[name] = c.get(name, 0) + n
+
+    def counters(self, rank):
+        with self._stats_lock:
+            return dict(self._counters[rank])
+
+    def reset_counters(self):
+        with self._stats_lock:
+            for c in self._counters:
+                c.clear()
+
+    # ------------------------------------------------------------------
+    # device error words
+
+    def poll_error(self, rank):
+        code = ctypes.c_int()
+        _lib.check(self._lib.sh_poll_error(self._handle, rank, ctypes.byref(code)))
+        return code.value
+
+    def check_errors(self, rank):
+        code = self.poll_error(rank)
+        if code:
+            what = {1: "AllGather chunk flag", 2: "ReduceScatter slot release",
+                    3: "ReduceScatter arrival counter", 4: "stream flag wait"}.get(code, "flag")
+            raise SynchronizationFault(
+                f"rank {rank}: device wait on {what} exceeded {self.spec.timeout_s} s")
+
+    def recover(self):
+        """Clear device error words and host rendezvous state (core.py:489-493)."""
+        import torch
+
+        for r in self.local_ranks:
+            torch.cuda.synchronize(self._dev_of(r))
+            _lib.check(self._lib.sh_clear_error(self._handle, r))
+        self._barrier_obj = _HostBarrier(len(self.local_ranks))
+
+    # ------------------------------------------------------------------
+    # epochs / reset
+
+    def _register_epochs(self, holder):
+        self._epoch_holders.append(holder)
+
+    def _request_reset(self, sigsets):
+        with self._reset_lock:
+            for s in sigsets:
+                self._reset_sets.add(s)
+
+    def _apply_resets(self):
+        """After a join every rank is past every flag of the finished calls,
+        so zeroing is race-free (the epoch protocol needs no reset in between;
+        this restores the reference's flag hygiene, collectives.py:67-69)."""
+        import torch
+
+        with self._reset_lock:
+            sets, self._reset_sets = self._reset_sets, set()
+        if not sets:
+            return
+        for r in self.local_ranks:
+            torch.cuda.synchronize(self._dev_of(r))
+            for s in sets:
+                self.zero_signals(r, s.base, s.count)
+            torch.cuda.synchronize(self._dev_of(r))
+        for holder in self._epoch_holders:
+            holder.reset_epochs_for(sets)
+
+    # ------------------------------------------------------------------
+    # running rank functions (reference core.py:449-547)
+
+    def _barrier(self, pe):
+        import torch
+
+        torch.cuda.synchronize(pe.device)
+        if self._dist:
+            import torch.distributed as dist
+
+            dist.barrier()
+        else:
+            self._barrier_obj.wait(self.spec.timeout_s * 4 + 30)
+
+    def _run_rank(self, fn, rank):
+        import torch
+
+        pe = self.pes[rank]
+        torch.cuda.set_device(pe.device)
+        s = pe.stream()
+        s.wait_stream(torch.cuda.current_stream(pe.device))
+        with torch.cuda.stream(s):
+            val = fn(pe)
+        s.synchronize()
+        self.check_errors(rank)
+        return val
+
+    def run(self, fn, timeout=None):
+        """Run ``fn(pe)`` on every local rank concurrently; per-rank results in
+        rank order.  Device work of each rank is drained before returning, and
+        any failure is aggregated into ``CollectiveFault``.
+
+        Ranks that share a process must not block on the GPU inside ``fn``
+        once they have issued a collective (``.cpu()``, ``.item()``, pageable
+        ``.to('cuda')``): the CUDA driver serialises pageable copies, so a rank
+        waiting on its stream there can hold back a sibling's launch that its
+        stream is waiting for.  Stage inputs first, return device tensors."""
+        if self._closed:
+            raise ConfigurationError("world is closed")
+        ranks = self.local_ranks
+        if len(ranks) == 1:
+            try:
+                res = [self._run_rank(fn, ranks[0])]
+            except BaseException as exc:  # noqa: BLE001 - aggregate like the reference
+                raise CollectiveFault(f"collective failed on ranks {ranks[0]}: "
+                                      f"{type(exc).__name__}: {exc}", {ranks[0]: exc}) from exc
+            self._apply_resets()
+            return res
+        self._ensure_workers()
+        for r in ranks:
+            self._jobs[r].append(fn)
+            self._job_ev[r].set()
+        wait_s = (timeout or self.spec.timeout_s) * 4.0 + 60.0
+        results, failures = {}, {}
+        for r in ranks:
+            if not self._done_ev[r].wait(wait_s):
+                failures[r] = TimeoutError(f"rank {r} did not finish")
+                continue
+            self._done_ev[r].clear()
+            ok, val = self._results[r]
+            if ok:
+                results[r] = val
+            else:
+                failures[r] = val
+        if failures:
+            raise CollectiveFault(
+                "collective failed on ranks "
+                + ", ".join(f"{r}: {type(e).__name__}: {e}" for r, e in sorted(failures.items())),
+                failures)
+        self._apply_resets()
+        return [results[r] for r in ranks]
+
+    def _ensure_workers(self):
+        if self._workers is not None:
+            return
+        self._jobs = {r: deque() for r in self.local_ranks}
+        self._job_ev = {r: threading.Event() for r in self.local_ranks}
+        self._done_ev = {r: threading.Event() for r in self.local_ranks}
+        self._results = {}
+        self._workers = []
+        for r in self.local_ranks:
+            t = threading.Thread(target=self._worker_loop, args=(r,), daemon=True, name=f"rank{r}")
+            t.start()
+            self._workers.append(t)
+
+    def _worker_loop(self, rank):
+        while True:
+            self._job_ev[rank].wait()
+            self._job_ev[rank].clear()
+            if self._closed:
+                return
+            while self._jobs[rank]:
+                fn = self._jobs[rank].popleft()
+                try:
+                    self._results[rank] = (True, self._run_rank(fn, rank))
+                except BaseException as exc:  # noqa: BLE001
+                    self._results[rank] = (False, exc)
+                self._done_ev[rank].set()
+
+    def close(self):
+        if self._closed:
+            return
+        self._closed = True
+        if self._workers:
+            for ev in self._job_ev.values():
+                ev.set()
+        if self._handle:
+            try:
+                import torch
+
+                for r in self.local_ranks:
+                    torch.cuda.synchronize(self._dev_of(r))
+            except Exception:  # noqa: BLE001
+                pass
+            self._lib.sh_world_destroy(self._handle)
+            self._handle = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def init_world(spec: WorldSpec, scheduler="free", seed=0) -> World:
+    """Single-process world: every rank a thread (reference core.py:565-567)."""
+    return World(spec, scheduler=scheduler, seed=seed)
+
+
+def exchange_ipc_handles(world: World, all_gather):
+    """Attach every peer slab: ``all_gather(bytes) -> list[bytes]`` is the
+    out-of-band exchange (torch.distributed.all_gather_object in practice,
+    any transport in tests).  One rank per process."""
+    lib = world._lib
+    size = lib.sh_ipc_handle_size()
+    buf = (ctypes.c_char * size)()
+    _lib.check(lib.sh_export_ipc_handle(world.handle, buf))
+    handles = all_gather(bytes(buf))
+    if len(handles) != world.world_size or any(len(h) != size for h in handles):
+        raise ConfigurationError("IPC handle exchange returned a malformed list")
+    blob = b"".join(handles)
+    arr = (ctypes.c_char * len(blob)).from_buffer_copy(blob)
+    _lib.check(lib.sh_import_ipc_handles(world.handle, arr))
+
+
+def init_world_dist(heap_bytes=1 << 30, signal_count=None, timeout_s=5.0, device=None) -> World:
+    """One process per GPU under torch.distributed (already initialised):
+    this process hosts rank ``dist.get_rank()`` on ``device`` (default
+    LOCAL_RANK).  Peers' slabs are mapped with CUDA IPC."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        raise ConfigurationError("torch.distributed is not initialised")
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", rank % max(1, torch.cuda.device_count())))
+    spec = WorldSpec(world_size=ws, heap_bytes=heap_bytes, signal_count=signal_count,
+                     timeout_s=timeout_s)
+    world = World(spec, _member=(rank, device))
+
+    def gather(b):
+        out = [None] * ws
+        dist.all_gather_object(out, b)
+        return out
+
+    if ws > 1:
+        exchange_ipc_handles(world, gather)
+    dist.barrier()
+    return world

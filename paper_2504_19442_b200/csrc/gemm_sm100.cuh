@@ -1,0 +1,411 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a with the two fused
+// tensor-parallel epilogues of the hot path:
+//
+//   MODE_AG : C[m, n] = concat_r(A_shard_r) @ B.  The TMA-producer warp gates
+//             every A tile of chunk c on the per-source flag ready[c] (set
+//             by the owner's push), so tiles of the local shard start at
+//             once and remote chunks are consumed as they land.
+//             Reference: pipelines.py:97-150 (ag_gemm), collectives.py:83-102.
+//   MODE_RS : rows of chunk d of (A @ B) are written as bf16 straight into
+//             rank d's staging slot `rank` (peer TMA store over NVLink) and
+//             a release-add on d's per-source counter publishes them.
+//             Reference: pipelines.py:179-216 (gemm_rs) + collectives.py:153-161.
+//
+// Layout: A is K-major (row-major m x k), B is MN-major (row-major k x n, the
+// reference's argument layout, pipelines.py:112).  Both are staged by TMA with
+// 128-byte swizzle.  A CTA pair (cta_group::2) computes a 256 x BN tile; each
+// CTA owns 128 rows of A and BN/2 columns of B in shared memory and 128 x BN
+// fp32 accumulator columns in TMEM (double buffered across tiles).
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
+// CTA) + TMEM allocator (both CTAs), warps 2..5 epilogue (TMEM -> regs ->
+// bf16 -> swizzled smem -> TMA store).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "ptx.cuh"
+
+namespace shb {
+
+constexpr int kMaxWorld = 16;
+constexpr int MODE_AG = 0;
+constexpr int MODE_RS = 1;
+
+struct TileParams {
+  int rows;       // rows per chunk (m / world)
+  int n, k;
+  int world, rank;
+  int mblk, nblk;  // m-blocks per chunk, n-blocks
+  int num_tiles;   // world * mblk * nblk
+  int group_m;     // raster group (m-blocks) for L2 reuse
+  int order[kMaxWorld];  // chunk visit order (reference swizzle.py)
+  uint64_t epoch;
+  const uint64_t* ready;              // AG: my pad, ready[src] (written by src)
+  uint64_t* rs_count[kMaxWorld];      // RS: &pad_d[reduction + rank]
+  const uint64_t* rs_free;            // RS: my pad, producer[d] >= epoch-1: d reduced last call
+  int* err;                           // host-mapped error word
+  uint64_t timeout_ns;
+};
+
+struct TensorMaps {
+  CUtensorMap a_own;  // AG: a_shard {k, rows}
+  CUtensorMap a_all;  // AG: gathered {k, rows, W}; RS: a {k, rows, W}
+  CUtensorMap b;      // {n, k}
+  CUtensorMap c;      // AG: C {n, rows, W}
+  CUtensorMap out[kMaxWorld];  // RS: dest d's staging slot `rank`, {n, rows}
+};
+
+__device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chunk, int& mb,
+                                            int& nb) {
+  const int per_chunk = p.mblk * p.nblk;
+  const int s = t / per_chunk;
+  const int w = t - s * per_chunk;
+  chunk = p.order[s];
+  const int gm = p.group_m;
+  const int span = gm * p.nblk;
+  const int group = w / span;
+  const int first_m = group * gm;
+  const int gsize = min(p.mblk - first_m, gm);
+  const int in = w - group * span;
+  mb = first_m + in % gsize;
+  nb = in / gsize;
+}
+
+template <int BN, int CG>
+struct GemmCfg {
+  static constexpr int BM = 128;  // rows per CTA (UMMA M per CTA)
+  static constexpr int BK = 64;   // 128 bytes of bf16: one swizzle atom row
+  static constexpr int BNC = BN / CG;  // B columns staged per CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BNC * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;
+  static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static_assert(BNC % 64 == 0, "per-CTA B tile must be a multiple of 64 columns");
+  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  static constexpr int stages_for_smem() {
+    return (220 * 1024 - EPI_BYTES) / STAGE_BYTES;
+  }
+  static constexpr int STAGES = stages_for_smem() > 8 ? 8 : stages_for_smem();
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+};
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi, bool fp16) {
+  if (fp16) {
+    __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, int CG, int MODE, bool FP16>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tp_kernel(const __grid_constant__ TensorMaps maps, const __grid_constant__ TileParams p) {
+  using C = GemmCfg<BN, CG>;
+  constexpr int BM = C::BM, BK = C::BK, BNC = C::BNC, STAGES = C::STAGES;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * C::A_BYTES;
+  uint8_t* sEpi = sB + STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cta_rank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = cta_rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&maps.a_all);
+    prefetch_tmap(&maps.b);
+    if (MODE == MODE_AG) {
+      prefetch_tmap(&maps.a_own);
+      prefetch_tmap(&maps.c);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], CG * 4);
+    }
+    fence_mbarrier_init();
+  }
+  if (warp == 2) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
+  const int num_kb = (p.k + BK - 1) / BK;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        int chunk, mb, nb;
+        decode_tile(p, t, chunk, mb, nb);
+        const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
+        const int col0 = nb * BN + (int)cta_rank * BNC;
+        const bool own = (MODE == MODE_AG) && chunk == p.rank;
+        if (MODE == MODE_AG && !own && !((landed >> chunk) & 1u)) {
+          // wait(ready[chunk]) of pipelines.py:130-141, as an acquire spin
+          spin_geq(p.ready + chunk, p.epoch, p.err, p.timeout_ns, 1);
+          fence_proxy_async_global();
+          landed |= 1u << chunk;
+        }
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a_dst = sA + stage * C::A_BYTES;
+          uint8_t* b_dst = sB + stage * C::B_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
+          const int kx = kb * BK;
+          if constexpr (CG == 1) {
+            if (own) tma_load_2d(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
+            else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+#pragma unroll
+            for (int j = 0; j < BNC / 64; ++j)
+              tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                          kEvictNormal);
+          } else {
+            if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
+            else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+#pragma unroll
+            for (int j = 0; j < BNC / 64; ++j)
+              tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                               kEvictNormal);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA) =====================
+    if (leader && lane == 0) {
+      constexpr uint32_t IDESC = umma_idesc_f16(BM * CG, BN, FP16 ? 0 : 1, /*a K-major*/ 0,
+                                                /*b MN-major*/ 1);
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait_cluster(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // A: K-major SW128, +32 B per 16-element K step.  SBO = 8 rows x 128 B.
+            const uint64_t ad = umma_desc(a_addr + kk * 32, 16, 1024, 2);
+            // B: MN-major SW128: 64-column atoms 8 KB apart (LBO), 8-row K
+            // groups 1 KB apart (SBO); +2 KB per 16-row K step.
+            const uint64_t bd = umma_desc(b_addr + kk * 2048, 64 * BK * 2, 1024, 2);
+            umma_f16<CG>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+          }
+          umma_commit<CG>(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit<CG>(&tfull[as]);
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
+    int buf = 0;
+    int it = 0;
+    uint32_t freed = 0;  // RS: destinations observed free for this epoch
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+      int chunk, mb, nb;
+      decode_tile(p, t, chunk, mb, nb);
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      const int row = mb * (BM * CG) + (int)cta_rank * BM + q * 32;  // first row of slab
+      const int n0 = nb * BN;
+      if (MODE == MODE_RS && !((freed >> chunk) & 1u)) {
+        // dest must have reduced the previous call before its slot is reused
+        if (lane == 0 && p.epoch > 1)
+          spin_geq(p.rs_free + chunk, p.epoch - 1, p.err, p.timeout_ns, 2);
+        __syncwarp();
+        freed |= 1u << chunk;
+      }
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+#pragma unroll 1
+      for (int j = 0; j < BN / 64; ++j) {
+        uint32_t v0[32], v1[32];
+        tmem_ld_32x32b_x32(t_row + j * 64, v0);
+        tmem_ld_32x32b_x32(t_row + j * 64 + 32, v1);
+        tmem_ld_wait();
+        if (j == BN / 64 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(&tempty[as], 0);
+            else mbar_arrive(&tempty[as]);
+          }
+        }
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* sb = stg + buf * 4096;
+        uint8_t* rowp = sb + lane * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t* src = (c < 4) ? &v0[c * 8] : &v1[(c - 4) * 8];
+          uint4 w;
+          w.x = pack2(__uint_as_float(src[0]), __uint_as_float(src[1]), FP16);
+          w.y = pack2(__uint_as_float(src[2]), __uint_as_float(src[3]), FP16);
+          w.z = pack2(__uint_as_float(src[4]), __uint_as_float(src[5]), FP16);
+          w.w = pack2(__uint_as_float(src[6]), __uint_as_float(src[7]), FP16);
+          *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) = w;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (MODE == MODE_AG) tma_store_3d(&maps.c, sb, n0 + j * 64, row, chunk);
+          else tma_store_2d(&maps.out[chunk], sb, n0 + j * 64, row);
+          bulk_commit();
+        }
+        buf ^= 1;
+      }
+      if constexpr (MODE == MODE_RS) {
+        if (lane == 0) {
+          // count the elements this warp actually delivered (TMA clips the
+          // ragged edges), so a chunk is complete at exactly rows*n per call
+          const int vr = max(0, min(32, p.rows - row));
+          const int vc = max(0, min(BN, p.n - n0));
+          bulk_wait<0>();
+          fence_proxy_async_global();
+          fence_acq_rel_sys();
+          red_add_release_sys(p.rs_count[chunk], (uint64_t)vr * (uint64_t)vc);
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ReduceScatter reduction: out = sum_{s ascending} staging[s] in fp32, stored
+// as bf16/fp16 (reference collectives.py:163-171; fixed ascending source
+// order keeps the float result reproducible).  Each CTA waits
+// for every source's element counter to reach epoch*rows*n first.
+template <bool FP16>
+__global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restrict__ staging,
+                                                        uint16_t* __restrict__ out,
+                                                        size_t slot_elems, int world,
+                                                        const uint64_t* counters, uint64_t target,
+                                                        int* err, uint64_t timeout_ns) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < world; ++s) spin_geq(counters + s, target, err, timeout_ns, 3);
+  }
+  __syncthreads();
+  const size_t nvec = slot_elems / 8;
+  const uint4* st = reinterpret_cast<const uint4*>(staging);
+  uint4* o = reinterpret_cast<uint4*>(out);
+  const size_t slot_vec = slot_elems / 8;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int s = 0; s < world; ++s) {
+      uint4 v = __ldcs(st + s * slot_vec + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float lo, hi;
+        if (FP16) {
+          __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
+          float2 f = __half22float2(h);
+          lo = f.x; hi = f.y;
+        } else {
+          __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
+          float2 f = __bfloat1622float2(h);
+          lo = f.x; hi = f.y;
+        }
+        acc[2 * e] += lo;
+        acc[2 * e + 1] += hi;
+      }
+    }
+    uint4 r;
+    r.x = pack2(acc[0], acc[1], FP16);
+    r.y = pack2(acc[2], acc[3], FP16);
+    r.z = pack2(acc[4], acc[5], FP16);
+    r.w = pack2(acc[6], acc[7], FP16);
+    __stcs(o + i, r);
+  }
+  // scalar tail (slot_elems % 8)
+  const size_t tail0 = nvec * 8;
+  for (size_t i = tail0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < slot_elems;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < world; ++s) {
+      uint16_t h = staging[s * slot_elems + i];
+      acc += FP16 ? __half2float(__ushort_as_half(h)) : __bfloat162float(__ushort_as_bfloat16(h));
+    }
+    out[i] = FP16 ? __half_as_ushort(__float2half_rn(acc))
+                  : __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+  }
+}
+
+// Flag publication: one release store per peer (the signal_op(SET) of
+// reference collectives.py:97 / :161 for a whole chunk).
+__global__ void flag_store_kernel(uint64_t* const* ptrs, int count, uint64_t value) {
+  int i = threadIdx.x;
+  if (i < count) {
+    __threadfence_system();
+    st_release_sys(ptrs[i], value);
+  }
+}
+
+struct FlagList {
+  uint64_t* ptr[kMaxWorld];
+};
+
+__global__ void flag_store_list_kernel(const __grid_constant__ FlagList l, int count,
+                                       uint64_t value) {
+  int i = threadIdx.x;
+  if (i < count) {
+    __threadfence_system();
+    st_release_sys(l.ptr[i], value);
+  }
+}
+
+// Stream-side wait on a local flag (used only when stream memory operations
+// are unavailable).
+__global__ void flag_wait_kernel(const uint64_t* flag, uint64_t target, int* err,
+                                 uint64_t timeout_ns) {
+  if (threadIdx.x == 0) spin_geq(flag, target, err, timeout_ns, 4);
+}
+
+}  // namespace shb

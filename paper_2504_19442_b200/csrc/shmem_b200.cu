@@ -1,0 +1,939 @@
+// Host side of the C ABI (include/shmem_b200.h): symmetric heap, flag/epoch
+// protocol, tensor-map construction and kernel launch for the fused
+// AllGather+GEMM and GEMM+ReduceScatter paths.
+//
+// Heap layout is the reference's (core.py:159-160, 242-261): every rank owns a
+// slab of `heap_bytes + 8*signal_count` bytes; symmetric handles are offsets
+// valid in every slab; signal word `sig` lives at slab + heap_bytes + 8*sig.
+// Here each slab is device memory on the rank's GPU and every other rank holds
+// a peer mapping of it (cudaDeviceEnablePeerAccess in one process, CUDA IPC
+// across processes), so a "remote write" is an NVLink store.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/shmem_b200.h"
+#include "gemm_sm100.cuh"
+
+using namespace shb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(SH_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),   \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// driver entry points (no link-time dependency on libcuda)
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_streamWaitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_writeValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+struct Driver {
+  PFN_encodeTiled encode = nullptr;
+  PFN_streamWaitValue64 wait64 = nullptr;
+  PFN_writeValue64 write64 = nullptr;
+  bool ok = false;
+  std::string why;
+};
+
+Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn) {
+      d.encode = reinterpret_cast<PFN_encodeTiled>(fn);
+      d.ok = true;
+    } else {
+      d.why = "cuTensorMapEncodeTiled unavailable";
+    }
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      d.wait64 = reinterpret_cast<PFN_streamWaitValue64>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      d.write64 = reinterpret_cast<PFN_writeValue64>(fn);
+  });
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// tile configuration
+
+std::atomic<int> g_force_bn{0};
+std::atomic<int> g_force_cg{0};
+
+int num_sms(int dev) {
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 148;
+  }
+  return cache[dev];
+}
+
+struct Cfg {
+  int bn, cg, grid, mblk, nblk, tiles;
+};
+
+Cfg choose_cfg(int rows, int world, int n, int sms) {
+  int cgs[2] = {2, 1};
+  int bns[2] = {256, 128};
+  Cfg best{};
+  double best_score = -1;
+  for (int ci = 0; ci < 2; ++ci) {
+    int cg = cgs[ci];
+    if (g_force_cg && g_force_cg != cg) continue;
+    if (!g_force_cg && cg == 1) continue;  // pairs by default
+    for (int bi = 0; bi < 2; ++bi) {
+      int bn = bns[bi];
+      if (g_force_bn && g_force_bn != bn) continue;
+      if (cg == 2 && bn < 128) continue;
+      int bm = 128 * cg;
+      int mblk = (rows + bm - 1) / bm;
+      int nblk = (n + bn - 1) / bn;
+      int tiles = world * mblk * nblk;
+      int max_clusters = sms / cg;
+      int clusters = tiles < max_clusters ? tiles : max_clusters;
+      int waves = (tiles + clusters - 1) / clusters;
+      double eff = double(tiles) / double(waves * clusters) * double(clusters * cg) / sms;
+      // useful-work fraction (ragged edges compute padding) times wave fill,
+      // with a small penalty for narrow tiles (more operand traffic per flop)
+      double useful = double(rows) * n / (double(mblk) * bm * nblk * bn);
+      double score = eff * useful * (bn == 256 ? 1.0 : 0.94);
+      if (score > best_score) {
+        best_score = score;
+        best = Cfg{bn, cg, clusters * cg, mblk, nblk, tiles};
+      }
+    }
+  }
+  return best;
+}
+
+// ---------------------------------------------------------------------------
+// tensor maps
+
+int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_t* dims,
+             const uint64_t* strides_bytes, const uint32_t* box) {
+  Driver& d = driver();
+  if (!d.ok) return fail(SH_ERR_CUDA, "%s", d.why.c_str());
+  cuuint64_t gd[3];
+  cuuint64_t gs[2];
+  cuuint32_t bx[3];
+  cuuint32_t es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  CUresult r = d.encode(m, dtype == SH_DTYPE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                  : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                        rank, const_cast<void*>(ptr), gd, gs, bx, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SH_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) ptr=%p dims=%llu,%llu", (int)r,
+                ptr, (unsigned long long)dims[0], (unsigned long long)dims[1]);
+  return SH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+
+template <int BN, int CG, int MODE, bool FP16>
+int launch_one(const TensorMaps& maps, const TileParams& p, int grid, cudaStream_t s) {
+  using C = GemmCfg<BN, CG>;
+  auto kern = gemm_tp_kernel<BN, CG, MODE, FP16>;
+  // smem attribute + carveout are set per device by preload_kernels()
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(192, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, p));
+  return SH_OK;
+}
+
+template <int MODE, bool FP16>
+int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaStream_t s) {
+  if (c.cg == 2) {
+    if (c.bn == 256) return launch_one<256, 2, MODE, FP16>(maps, p, c.grid, s);
+    return launch_one<128, 2, MODE, FP16>(maps, p, c.grid, s);
+  }
+  if (c.bn == 256) return launch_one<256, 1, MODE, FP16>(maps, p, c.grid, s);
+  return launch_one<128, 1, MODE, FP16>(maps, p, c.grid, s);
+}
+
+template <int MODE>
+int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParams& p,
+                cudaStream_t s) {
+  if (dtype == SH_DTYPE_FP16) return launch_mode<MODE, true>(c, maps, p, s);
+  return launch_mode<MODE, false>(c, maps, p, s);
+}
+
+// Load every kernel of this library on `dev` now.  With CUDA lazy loading a
+// first launch may need a context-wide synchronisation, which deadlocks
+// against a kernel of another rank that is spinning on a flag this launch
+// is supposed to set (ranks sharing one GPU).
+template <int BN, int CG, int MODE, bool FP16>
+cudaError_t preload_one() {
+  cudaFuncAttributes a;
+  auto kern = gemm_tp_kernel<BN, CG, MODE, FP16>;
+  cudaError_t e = cudaFuncGetAttributes(&a, kern);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              GemmCfg<BN, CG>::SMEM_BYTES);
+}
+
+template <int MODE, bool FP16>
+cudaError_t preload_mode() {
+  cudaError_t e;
+  if ((e = preload_one<256, 2, MODE, FP16>())) return e;
+  if ((e = preload_one<128, 2, MODE, FP16>())) return e;
+  if ((e = preload_one<256, 1, MODE, FP16>())) return e;
+  return preload_one<128, 1, MODE, FP16>();
+}
+
+int preload_kernels(int dev) {
+  CUDA_TRY(cudaSetDevice(dev));
+  CUDA_TRY((preload_mode<MODE_AG, false>()));
+  CUDA_TRY((preload_mode<MODE_AG, true>()));
+  CUDA_TRY((preload_mode<MODE_RS, false>()));
+  CUDA_TRY((preload_mode<MODE_RS, true>()));
+  // Small kernels that may spin (or sit next to a spinning kernel) ask for
+  // the max-shared-memory carveout: an SM configured for L1 cannot take a
+  // GEMM CTA (~225 KB smem) until it drains, and a drained SM is exactly
+  // what a spinning reduction would be waiting for.
+  const void* small[] = {reinterpret_cast<const void*>(rs_reduce_kernel<false>),
+                         reinterpret_cast<const void*>(rs_reduce_kernel<true>),
+                         reinterpret_cast<const void*>(flag_store_kernel),
+                         reinterpret_cast<const void*>(flag_store_list_kernel),
+                         reinterpret_cast<const void*>(flag_wait_kernel)};
+  for (const void* f : small) {
+    cudaFuncAttributes a;
+    CUDA_TRY(cudaFuncGetAttributes(&a, f));
+    CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+  }
+  return SH_OK;
+}
+
+int ensure_preloaded(int dev) {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  if (dev < 0 || dev >= 64) return fail(SH_ERR_ARG, "device %d", dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return SH_OK;
+  int cur = 0;
+  CUDA_TRY(cudaGetDevice(&cur));
+  int rc = preload_kernels(dev);
+  CUDA_TRY(cudaSetDevice(cur));
+  if (rc) return rc;
+  done[dev] = true;
+  return SH_OK;
+}
+
+int check_shape(int m, int n, int k, int world, int dtype) {
+  if (m < 1 || n < 1 || k < 1) return fail(SH_ERR_ARG, "m, n, k must be >= 1");
+  if (world < 1 || world > SH_MAX_WORLD)
+    return fail(SH_ERR_ARG, "world %d outside 1..%d", world, SH_MAX_WORLD);
+  if (m % world) return fail(SH_ERR_ARG, "M=%d not divisible by world %d", m, world);
+  if (dtype != SH_DTYPE_BF16 && dtype != SH_DTYPE_FP16)
+    return fail(SH_ERR_ARG, "dtype %d not supported (bf16/fp16 only)", dtype);
+  if (n % 8 || k % 8)
+    return fail(SH_ERR_ARG, "n (%d) and k (%d) must be multiples of 8 (16-byte TMA rows)", n, k);
+  return SH_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// world
+
+struct RankState {
+  int rank = -1;
+  int device = -1;
+  void* slab = nullptr;      // own slab (device memory on `device`)
+  bool own_alloc = false;
+  void* peer[SH_MAX_WORLD] = {nullptr};  // every slab as seen from this rank's device
+  bool ipc_opened[SH_MAX_WORLD] = {false};
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_done = nullptr;
+  int* err_host = nullptr;
+  int* err_dev = nullptr;
+  bool shares_gpu = false;  // another rank of this process uses the same device
+};
+
+struct sh_world {
+  int world = 0;
+  size_t heap_bytes = 0;
+  int signal_count = 0;
+  size_t stride = 0;
+  uint64_t timeout_ns = 0;
+  bool member = false;
+  int member_rank = -1;
+  std::mutex mu;
+  size_t heap_cursor = 0;
+  int sig_cursor = 0;
+  RankState r[SH_MAX_WORLD];
+};
+
+namespace {
+
+int init_rank_common(sh_world* w, RankState& rs) {
+  int rc = ensure_preloaded(rs.device);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(rs.device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&rs.comm, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_in, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&rs.err_host), sizeof(int), cudaHostAllocMapped));
+  *rs.err_host = 0;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&rs.err_dev), rs.err_host, 0));
+  (void)w;
+  return SH_OK;
+}
+
+int validate_world_args(int world_size, size_t heap_bytes, int* signal_count) {
+  if (world_size < 1 || world_size > SH_MAX_WORLD)
+    return fail(SH_ERR_CONFIG, "world_size %d outside 1..%d", world_size, SH_MAX_WORLD);
+  if (heap_bytes == 0) return fail(SH_ERR_CONFIG, "heap_bytes must be > 0");
+  if (*signal_count <= 0) *signal_count = (4 * world_size > 64) ? 4 * world_size : 64;
+  if (*signal_count < world_size) return fail(SH_ERR_CONFIG, "signal_count must be >= world_size");
+  return SH_OK;
+}
+
+RankState* rank_of(sh_world* w, int rank) {
+  if (!w || rank < 0 || rank >= w->world) return nullptr;
+  if (w->member && rank != w->member_rank) return nullptr;
+  return &w->r[rank];
+}
+
+inline uint64_t* sig_addr(sh_world* w, const RankState& rs, int peer, int sig) {
+  return reinterpret_cast<uint64_t*>(static_cast<char*>(rs.peer[peer]) + w->heap_bytes +
+                                     8 * (size_t)sig);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+int stream_wait_geq(RankState& rs, cudaStream_t s, const uint64_t* flag, uint64_t target,
+                    uint64_t timeout_ns) {
+  if (target == 0) return SH_OK;  // every flag is >= 0
+  Driver& d = driver();
+  if (env_int("SHB_WAIT_KERNEL", 0)) {
+    flag_wait_kernel<<<1, 32, 0, s>>>(flag, target, rs.err_dev, timeout_ns);
+    CUDA_TRY(cudaGetLastError());
+    return SH_OK;
+  }
+  if (d.wait64) {
+    CUresult r = d.wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag),
+                          target, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r == CUDA_SUCCESS) return SH_OK;
+  }
+  flag_wait_kernel<<<1, 32, 0, s>>>(flag, target, rs.err_dev, timeout_ns);
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+int store_flags(cudaStream_t s, uint64_t* const* ptrs, int count, uint64_t value) {
+  if (count <= 0) return SH_OK;
+  // Stream memory operation (executed by the GPU front end, no SM needed,
+  // implicit memory barrier before the write = data-before-flag); the
+  // one-warp release-store kernel is the fallback.
+  Driver& d = driver();
+  if (d.write64 && !env_int("SHB_FLAG_KERNEL", 0)) {
+    bool ok = true;
+    for (int i = 0; i < count && ok; ++i)
+      ok = d.write64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(ptrs[i]), value,
+                     CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS;
+    if (ok) return SH_OK;
+    if (count > 1) return fail(SH_ERR_CUDA, "cuStreamWriteValue64 failed midway");
+  }
+  FlagList l;
+  for (int i = 0; i < count; ++i) l.ptr[i] = ptrs[i];
+  flag_store_list_kernel<<<1, 32, 0, s>>>(l, count, value);
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sh_version(void) { return 1; }
+
+const char* sh_last_error(void) { return g_err.c_str(); }
+
+int sh_world_create(int world_size, const int* devices, size_t heap_bytes, int signal_count,
+                    double timeout_s, sh_world** out) {
+  if (!out) return fail(SH_ERR_ARG, "out is NULL");
+  int rc = validate_world_args(world_size, heap_bytes, &signal_count);
+  if (rc) return rc;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  auto* w = new sh_world();
+  w->world = world_size;
+  w->heap_bytes = heap_bytes;
+  w->signal_count = signal_count;
+  w->stride = (heap_bytes + 8 * (size_t)signal_count + 255) & ~size_t(255);
+  w->timeout_ns = (uint64_t)(timeout_s > 0 ? timeout_s * 1e9 : 5e9);
+  for (int r = 0; r < world_size; ++r) {
+    RankState& rs = w->r[r];
+    rs.rank = r;
+    rs.device = devices ? devices[r] : (ndev ? r % ndev : 0);
+    if (rs.device < 0 || rs.device >= ndev) {
+      delete w;
+      return fail(SH_ERR_CONFIG, "rank %d: device %d not present (%d GPUs)", r, rs.device, ndev);
+    }
+    if ((rc = init_rank_common(w, rs))) { delete w; return rc; }
+    cudaError_t e = cudaMalloc(&rs.slab, w->stride);
+    if (e != cudaSuccess) {
+      delete w;
+      return fail(SH_ERR_ALLOC, "cudaMalloc(%zu) for rank %d slab: %s", w->stride, r,
+                  cudaGetErrorString(e));
+    }
+    rs.own_alloc = true;
+    CUDA_TRY(cudaMemset(rs.slab, 0, w->stride));
+  }
+  // peer mappings: all devices that host ranks see each other over NVLink
+  for (int a = 0; a < world_size; ++a)
+    for (int b = 0; b < world_size; ++b) {
+      int da = w->r[a].device, db = w->r[b].device;
+      if (da != db) {
+        int can = 0;
+        CUDA_TRY(cudaDeviceCanAccessPeer(&can, da, db));
+        if (!can) {
+          delete w;
+          return fail(SH_ERR_CONFIG, "device %d cannot access peer %d", da, db);
+        }
+        CUDA_TRY(cudaSetDevice(da));
+        cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          delete w;
+          return fail(SH_ERR_CUDA, "enable peer %d->%d: %s", da, db, cudaGetErrorString(e));
+        }
+        cudaGetLastError();
+      }
+      w->r[a].peer[b] = w->r[b].slab;
+    }
+  for (int r = 0; r < world_size; ++r) {
+    for (int q = 0; q < world_size; ++q)
+      if (q != r && w->r[q].device == w->r[r].device) w->r[r].shares_gpu = true;
+    CUDA_TRY(cudaSetDevice(w->r[r].device));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  *out = w;
+  return SH_OK;
+}
+
+int sh_world_create_member(int world_size, int rank, int device, size_t heap_bytes,
+                           int signal_count, double timeout_s, sh_world** out) {
+  if (!out) return fail(SH_ERR_ARG, "out is NULL");
+  int rc = validate_world_args(world_size, heap_bytes, &signal_count);
+  if (rc) return rc;
+  if (rank < 0 || rank >= world_size) return fail(SH_ERR_CONFIG, "rank %d outside world", rank);
+  auto* w = new sh_world();
+  w->world = world_size;
+  w->heap_bytes = heap_bytes;
+  w->signal_count = signal_count;
+  w->stride = (heap_bytes + 8 * (size_t)signal_count + 255) & ~size_t(255);
+  w->timeout_ns = (uint64_t)(timeout_s > 0 ? timeout_s * 1e9 : 5e9);
+  w->member = true;
+  w->member_rank = rank;
+  RankState& rs = w->r[rank];
+  rs.rank = rank;
+  rs.device = device;
+  if ((rc = init_rank_common(w, rs))) { delete w; return rc; }
+  cudaError_t e = cudaMalloc(&rs.slab, w->stride);
+  if (e != cudaSuccess) {
+    delete w;
+    return fail(SH_ERR_ALLOC, "cudaMalloc(%zu): %s", w->stride, cudaGetErrorString(e));
+  }
+  rs.own_alloc = true;
+  CUDA_TRY(cudaMemset(rs.slab, 0, w->stride));
+  CUDA_TRY(cudaDeviceSynchronize());
+  rs.peer[rank] = rs.slab;
+  *out = w;
+  return SH_OK;
+}
+
+int sh_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int sh_export_ipc_handle(sh_world* w, void* handle_out) {
+  if (!w || !w->member || !handle_out) return fail(SH_ERR_ARG, "export needs a member world");
+  RankState& rs = w->r[w->member_rank];
+  CUDA_TRY(cudaSetDevice(rs.device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, rs.slab));
+  memcpy(handle_out, &h, sizeof(h));
+  return SH_OK;
+}
+
+int sh_import_ipc_handles(sh_world* w, const void* handles) {
+  if (!w || !w->member || !handles) return fail(SH_ERR_ARG, "import needs a member world");
+  RankState& rs = w->r[w->member_rank];
+  CUDA_TRY(cudaSetDevice(rs.device));
+  const char* hp = static_cast<const char*>(handles);
+  for (int p = 0; p < w->world; ++p) {
+    if (p == w->member_rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hp + p * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    rs.peer[p] = ptr;
+    rs.ipc_opened[p] = true;
+  }
+  return SH_OK;
+}
+
+int sh_world_destroy(sh_world* w) {
+  if (!w) return SH_OK;
+  for (int r = 0; r < w->world; ++r) {
+    RankState& rs = w->r[r];
+    if (rs.device < 0) continue;
+    cudaSetDevice(rs.device);
+    cudaDeviceSynchronize();
+    for (int p = 0; p < w->world; ++p)
+      if (rs.ipc_opened[p] && rs.peer[p]) cudaIpcCloseMemHandle(rs.peer[p]);
+    if (rs.own_alloc && rs.slab) cudaFree(rs.slab);
+    if (rs.comm) cudaStreamDestroy(rs.comm);
+    if (rs.ev_in) cudaEventDestroy(rs.ev_in);
+    if (rs.ev_done) cudaEventDestroy(rs.ev_done);
+    if (rs.err_host) cudaFreeHost(rs.err_host);
+  }
+  delete w;
+  return SH_OK;
+}
+
+int sh_alloc(sh_world* w, size_t nbytes, size_t align, size_t* offset) {
+  if (!w || !offset) return fail(SH_ERR_ARG, "null argument");
+  if (align < 1 || (align & (align - 1)))
+    return fail(SH_ERR_ARG, "alignment %zu is not a power of two", align);
+  std::lock_guard<std::mutex> g(w->mu);
+  size_t off = (w->heap_cursor + align - 1) & ~(align - 1);
+  if (off + nbytes > w->heap_bytes)
+    return fail(SH_ERR_ALLOC, "heap exhausted: need %zu at %zu, slab is %zu", nbytes, off,
+                w->heap_bytes);
+  w->heap_cursor = off + nbytes;
+  *offset = off;
+  return SH_OK;
+}
+
+int sh_alloc_signals(sh_world* w, int count, int* base) {
+  if (!w || !base) return fail(SH_ERR_ARG, "null argument");
+  if (count < 0) return fail(SH_ERR_ARG, "negative signal allocation");
+  std::lock_guard<std::mutex> g(w->mu);
+  if (w->sig_cursor + count > w->signal_count)
+    return fail(SH_ERR_ALLOC, "signal pad exhausted: need %d at %d, pad is %d", count,
+                w->sig_cursor, w->signal_count);
+  *base = w->sig_cursor;
+  w->sig_cursor += count;
+  return SH_OK;
+}
+
+int sh_heap_ptr(sh_world* w, int rank, int peer, size_t offset, void** ptr) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs || !ptr) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (peer < 0 || peer >= w->world || !rs->peer[peer])
+    return fail(SH_ERR_ARG, "peer %d out of range (world %d)", peer, w->world);
+  if (offset > w->heap_bytes) return fail(SH_ERR_ARG, "offset %zu outside heap", offset);
+  *ptr = static_cast<char*>(rs->peer[peer]) + offset;
+  return SH_OK;
+}
+
+int sh_signal_ptr(sh_world* w, int rank, int peer, int sig, void** ptr) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs || !ptr) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (peer < 0 || peer >= w->world || !rs->peer[peer])
+    return fail(SH_ERR_ARG, "peer %d out of range (world %d)", peer, w->world);
+  if (sig < 0 || sig >= w->signal_count)
+    return fail(SH_ERR_ARG, "signal %d out of pad of %d", sig, w->signal_count);
+  *ptr = sig_addr(w, *rs, peer, sig);
+  return SH_OK;
+}
+
+int sh_read_signals(sh_world* w, int rank, int base, int count, uint64_t* out_host) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs || !out_host) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (base < 0 || count < 0 || base + count > w->signal_count)
+    return fail(SH_ERR_ARG, "signals [%d, %d) outside pad of %d", base, base + count,
+                w->signal_count);
+  CUDA_TRY(cudaSetDevice(rs->device));
+  CUDA_TRY(cudaMemcpy(out_host, sig_addr(w, *rs, rank, base), 8 * (size_t)count,
+                      cudaMemcpyDeviceToHost));
+  return SH_OK;
+}
+
+int sh_reset_signals(sh_world* w, int rank, int base, int count, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (base < 0 || count < 0 || base + count > w->signal_count)
+    return fail(SH_ERR_ARG, "signals [%d, %d) outside pad of %d", base, base + count,
+                w->signal_count);
+  CUDA_TRY(cudaSetDevice(rs->device));
+  CUDA_TRY(cudaMemsetAsync(sig_addr(w, *rs, rank, base), 0, 8 * (size_t)count,
+                           static_cast<cudaStream_t>(stream)));
+  return SH_OK;
+}
+
+int sh_poll_error(sh_world* w, int rank, int* code) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs || !code) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  *code = *reinterpret_cast<volatile int*>(rs->err_host);
+  return SH_OK;
+}
+
+int sh_clear_error(sh_world* w, int rank) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  *reinterpret_cast<volatile int*>(rs->err_host) = 0;
+  return SH_OK;
+}
+
+int sh_set_tile_config(int bn, int cta_group) {
+  if (bn != 0 && bn != 128 && bn != 256) return fail(SH_ERR_ARG, "bn must be 0, 128 or 256");
+  if (cta_group < 0 || cta_group > 2) return fail(SH_ERR_ARG, "cta_group must be 0, 1 or 2");
+  g_force_bn = bn;
+  g_force_cg = cta_group;
+  return SH_OK;
+}
+
+int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Cfg c = choose_cfg(rows, world, n, num_sms(dev));
+  if (bn) *bn = c.bn;
+  if (cta_group) *cta_group = c.cg;
+  if (grid) *grid = c.grid;
+  return SH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plain GEMM core (TP = 1)
+
+int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream) {
+  int rc = check_shape(m, n, k, 1, dtype);
+  if (rc) return rc;
+  if (!a || !b || !c) return fail(SH_ERR_ARG, "null tensor");
+  if (!aligned16(a) || !aligned16(b) || !aligned16(c))
+    return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if ((rc = ensure_preloaded(dev))) return rc;
+  Cfg cfg = choose_cfg(m, 1, n, num_sms(dev));
+  TensorMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  const uint64_t es = 2;
+  {
+    uint64_t d[2] = {(uint64_t)k, (uint64_t)m}, s[1] = {(uint64_t)k * es};
+    uint32_t bx[2] = {64, 128};
+    if ((rc = make_map(&maps.a_own, dtype, a, 2, d, s, bx))) return rc;
+    uint64_t d3[3] = {(uint64_t)k, (uint64_t)m, 1}, s3[2] = {(uint64_t)k * es, (uint64_t)m * k * es};
+    uint32_t bx3[3] = {64, 128, 1};
+    if ((rc = make_map(&maps.a_all, dtype, a, 3, d3, s3, bx3))) return rc;
+  }
+  {
+    uint64_t d[2] = {(uint64_t)n, (uint64_t)k}, s[1] = {(uint64_t)n * es};
+    uint32_t bx[2] = {64, 64};
+    if ((rc = make_map(&maps.b, dtype, b, 2, d, s, bx))) return rc;
+  }
+  {
+    uint64_t d3[3] = {(uint64_t)n, (uint64_t)m, 1}, s3[2] = {(uint64_t)n * es, (uint64_t)m * n * es};
+    uint32_t bx3[3] = {64, 32, 1};
+    if ((rc = make_map(&maps.c, dtype, c, 3, d3, s3, bx3))) return rc;
+  }
+  TileParams p;
+  memset(&p, 0, sizeof(p));
+  p.rows = m;
+  p.n = n;
+  p.k = k;
+  p.world = 1;
+  p.rank = 0;
+  p.mblk = cfg.mblk;
+  p.nblk = cfg.nblk;
+  p.num_tiles = cfg.tiles;
+  p.group_m = 8;
+  p.order[0] = 0;
+  p.epoch = 1;
+  p.timeout_ns = 5000000000ull;
+  return launch_gemm<MODE_AG>(dtype, cfg, maps, p, static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------------------
+// fused AllGather + GEMM
+
+int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* c,
+               size_t gathered_off, int ready_base, int done_base, int m, int n, int k, int dtype,
+               const int* chunk_order, uint64_t epoch, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  const int W = w->world;
+  int rc = check_shape(m, n, k, W, dtype);
+  if (rc) return rc;
+  if (!a_shard || !b || !c || !chunk_order) return fail(SH_ERR_ARG, "null argument");
+  if (!aligned16(a_shard) || !aligned16(b) || !aligned16(c))
+    return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
+  if (epoch < 1) return fail(SH_ERR_ARG, "epoch must be >= 1");
+  const int rows = m / W;
+  const uint64_t es = 2;
+  const size_t chunk_bytes = (size_t)rows * k * es;
+  if (gathered_off % 16) return fail(SH_ERR_ARG, "gather buffer must be 16-byte aligned");
+  if (gathered_off + (size_t)W * chunk_bytes > w->heap_bytes)
+    return fail(SH_ERR_ARG, "gather buffer [%zu, +%zu) outside heap of %zu", gathered_off,
+                (size_t)W * chunk_bytes, w->heap_bytes);
+  if (ready_base < 0 || ready_base + W > w->signal_count || done_base < 0 ||
+      done_base + W > w->signal_count)
+    return fail(SH_ERR_ARG, "signal sets outside pad");
+  {
+    unsigned seen = 0;
+    for (int i = 0; i < W; ++i) {
+      int ch = chunk_order[i];
+      if (ch < 0 || ch >= W || (seen >> ch & 1u))
+        return fail(SH_ERR_ARG, "chunk order is not a permutation of 0..%d", W - 1);
+      seen |= 1u << ch;
+    }
+  }
+  CUDA_TRY(cudaSetDevice(rs->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = rs->device;
+  Cfg cfg = choose_cfg(rows, W, n, num_sms(dev));
+
+  // ---- comm half: push own shard into every rank's slot `rank`
+  // (allgather_push_intra, collectives.py:95-97).  Copy engine, in the order
+  // peers consume it under the ring schedule (peer p wants chunk `rank` at
+  // step (rank-p) mod W), after p finished reading the previous call.
+  // Ranks with a GPU of their own push on a side stream (copy engine), so
+  // the GEMM starts on the local shard while the pushes are in flight.
+  // Ranks sharing a GPU push on the caller's stream ahead of the GEMM: a
+  // side stream's copies could otherwise be queued behind another rank's
+  // spinning GEMM on the same device (measured: 13/30 W=8 runs stalled).
+  const bool push_on_main = rs->shares_gpu || env_int("SHB_PUSH_ON_MAIN", 0) != 0;
+  cudaStream_t cs = push_on_main ? s : rs->comm;
+  if (!push_on_main) {
+    CUDA_TRY(cudaEventRecord(rs->ev_in, s));
+    CUDA_TRY(cudaStreamWaitEvent(rs->comm, rs->ev_in, 0));
+  }
+  char* own_gathered = static_cast<char*>(rs->peer[rank]) + gathered_off;
+  for (int step = 1; step < W; ++step) {
+    int p = (rank - step + W) % W;
+    if ((rc = stream_wait_geq(*rs, cs, sig_addr(w, *rs, rank, done_base + p), epoch - 1,
+                              w->timeout_ns)))
+      return rc;
+    char* dst = static_cast<char*>(rs->peer[p]) + gathered_off + (size_t)rank * chunk_bytes;
+    CUDA_TRY(cudaMemcpyAsync(dst, a_shard, chunk_bytes, cudaMemcpyDeviceToDevice, cs));
+    uint64_t* f = sig_addr(w, *rs, p, ready_base + rank);
+    if ((rc = store_flags(cs, &f, 1, epoch))) return rc;
+  }
+  // own slot (read by nobody during the call; the gemm reads a_shard directly)
+  CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
+                           cudaMemcpyDeviceToDevice, cs));
+
+  // ---- compute half on the caller's stream
+  TensorMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  {
+    uint64_t d[2] = {(uint64_t)k, (uint64_t)rows}, st[1] = {(uint64_t)k * es};
+    uint32_t bx[2] = {64, 128};
+    if ((rc = make_map(&maps.a_own, dtype, a_shard, 2, d, st, bx))) return rc;
+    uint64_t d3[3] = {(uint64_t)k, (uint64_t)rows, (uint64_t)W},
+             s3[2] = {(uint64_t)k * es, (uint64_t)chunk_bytes};
+    uint32_t bx3[3] = {64, 128, 1};
+    if ((rc = make_map(&maps.a_all, dtype, own_gathered, 3, d3, s3, bx3))) return rc;
+  }
+  {
+    uint64_t d[2] = {(uint64_t)n, (uint64_t)k}, st[1] = {(uint64_t)n * es};
+    uint32_t bx[2] = {64, 64};
+    if ((rc = make_map(&maps.b, dtype, b, 2, d, st, bx))) return rc;
+  }
+  {
+    uint64_t d3[3] = {(uint64_t)n, (uint64_t)rows, (uint64_t)W},
+             s3[2] = {(uint64_t)n * es, (uint64_t)rows * n * es};
+    uint32_t bx3[3] = {64, 32, 1};
+    if ((rc = make_map(&maps.c, dtype, c, 3, d3, s3, bx3))) return rc;
+  }
+  TileParams p;
+  memset(&p, 0, sizeof(p));
+  p.rows = rows;
+  p.n = n;
+  p.k = k;
+  p.world = W;
+  p.rank = rank;
+  p.mblk = cfg.mblk;
+  p.nblk = cfg.nblk;
+  p.num_tiles = cfg.tiles;
+  p.group_m = 8;
+  for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
+  p.epoch = epoch;
+  p.ready = sig_addr(w, *rs, rank, ready_base);
+  p.err = rs->err_dev;
+  p.timeout_ns = w->timeout_ns;
+  if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s))) return rc;
+
+  // ---- publish "finished reading my gather buffer" to every peer, then
+  // join the comm stream so the call completes only when a_shard is free.
+  if (W > 1) {
+    uint64_t* fl[SH_MAX_WORLD];
+    int cnt = 0;
+    for (int q = 0; q < W; ++q)
+      if (q != rank) fl[cnt++] = sig_addr(w, *rs, q, done_base + rank);
+    if ((rc = store_flags(s, fl, cnt, epoch))) return rc;
+  }
+  if (!push_on_main) {
+    CUDA_TRY(cudaEventRecord(rs->ev_done, rs->comm));
+    CUDA_TRY(cudaStreamWaitEvent(s, rs->ev_done, 0));
+  }
+  return SH_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused GEMM + ReduceScatter
+
+int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
+               size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
+               int dtype, const int* chunk_order, uint64_t epoch, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  const int W = w->world;
+  int rc = check_shape(m, n, k, W, dtype);
+  if (rc) return rc;
+  if (!a || !b || !out || !chunk_order) return fail(SH_ERR_ARG, "null argument");
+  if (!aligned16(a) || !aligned16(b) || !aligned16(out))
+    return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
+  if (epoch < 1) return fail(SH_ERR_ARG, "epoch must be >= 1");
+  const int rows = m / W;
+  const uint64_t es = 2;
+  const size_t slot_bytes = (size_t)rows * n * es;
+  if (staging_off % 16) return fail(SH_ERR_ARG, "staging buffer must be 16-byte aligned");
+  if (staging_off + (size_t)W * slot_bytes > w->heap_bytes)
+    return fail(SH_ERR_ARG, "staging [%zu, +%zu) outside heap of %zu", staging_off,
+                (size_t)W * slot_bytes, w->heap_bytes);
+  if (producer_base < 0 || producer_base + W > w->signal_count || reduction_base < 0 ||
+      reduction_base + W > w->signal_count)
+    return fail(SH_ERR_ARG, "signal sets outside pad");
+  {
+    unsigned seen = 0;
+    for (int i = 0; i < W; ++i) {
+      int ch = chunk_order[i];
+      if (ch < 0 || ch >= W || (seen >> ch & 1u))
+        return fail(SH_ERR_ARG, "chunk order is not a permutation of 0..%d", W - 1);
+      seen |= 1u << ch;
+    }
+  }
+  CUDA_TRY(cudaSetDevice(rs->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device));
+
+  TensorMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  {
+    uint64_t d3[3] = {(uint64_t)k, (uint64_t)rows, (uint64_t)W},
+             s3[2] = {(uint64_t)k * es, (uint64_t)rows * k * es};
+    uint32_t bx3[3] = {64, 128, 1};
+    if ((rc = make_map(&maps.a_all, dtype, a, 3, d3, s3, bx3))) return rc;
+  }
+  {
+    uint64_t d[2] = {(uint64_t)n, (uint64_t)k}, st[1] = {(uint64_t)n * es};
+    uint32_t bx[2] = {64, 64};
+    if ((rc = make_map(&maps.b, dtype, b, 2, d, st, bx))) return rc;
+  }
+  for (int d = 0; d < W; ++d) {
+    // rank d's staging slot `rank` (collectives.py:160: dst_off = rank*chunk_bytes)
+    char* dst = static_cast<char*>(rs->peer[d]) + staging_off + (size_t)rank * slot_bytes;
+    uint64_t dd[2] = {(uint64_t)n, (uint64_t)rows}, st[1] = {(uint64_t)n * es};
+    uint32_t bx[2] = {64, 32};
+    if ((rc = make_map(&maps.out[d], dtype, dst, 2, dd, st, bx))) return rc;
+  }
+  TileParams p;
+  memset(&p, 0, sizeof(p));
+  p.rows = rows;
+  p.n = n;
+  p.k = k;
+  p.world = W;
+  p.rank = rank;
+  p.mblk = cfg.mblk;
+  p.nblk = cfg.nblk;
+  p.num_tiles = cfg.tiles;
+  p.group_m = 8;
+  for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
+  p.epoch = epoch;
+  for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);
+  p.rs_free = sig_addr(w, *rs, rank, producer_base);
+  p.err = rs->err_dev;
+  p.timeout_ns = w->timeout_ns;
+  if ((rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s))) return rc;
+
+  // reduction of my W staging slots in ascending source order
+  const uint16_t* staging =
+      reinterpret_cast<const uint16_t*>(static_cast<char*>(rs->peer[rank]) + staging_off);
+  const size_t slot_elems = (size_t)rows * n;
+  const uint64_t target = epoch * (uint64_t)slot_elems;
+  int sms = num_sms(rs->device);
+  size_t nvec = (slot_elems + 7) / 8;
+  int grid = (int)std::min<size_t>((nvec + 255) / 256, (size_t)sms * 4);
+  if (grid < 1) grid = 1;
+  const uint64_t* counters = sig_addr(w, *rs, rank, reduction_base);
+  if (dtype == SH_DTYPE_FP16)
+    rs_reduce_kernel<true><<<grid, 256, 0, s>>>(staging, static_cast<uint16_t*>(out), slot_elems,
+                                                W, counters, target, rs->err_dev, w->timeout_ns);
+  else
+    rs_reduce_kernel<false><<<grid, 256, 0, s>>>(staging, static_cast<uint16_t*>(out), slot_elems,
+                                                 W, counters, target, rs->err_dev, w->timeout_ns);
+  CUDA_TRY(cudaGetLastError());
+
+  // publish "reduced epoch" to every rank (incl. self): frees my staging
+  // slots for the next call (the join of collectives.py:1-10, made a flag)
+  uint64_t* fl[SH_MAX_WORLD];
+  for (int q = 0; q < W; ++q) fl[q] = sig_addr(w, *rs, q, producer_base + rank);
+  return store_flags(s, fl, W, epoch);
+}
+
+}  // extern "C"

@@ -1,0 +1,326 @@
+"""ag_gemm / gemm_rs on the GPU, written like the reference's own suite
+(/root/reference/pkg/tests/test_pipelines.py): identity shards give back B,
+random integer inputs match the dense oracle bit-exactly, schedule
+invariance, shape errors -> ArgumentError inside CollectiveFault, RS all-ones
+pattern, world of one.  Ranks are threads of one process (the reference's
+model); on a one-GPU box all W ranks share cuda:0, each on its own stream, and
+every "remote" store or flag goes through the same peer-pointer path the
+multi-GPU world uses."""
+
+import contextlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import minishmem_oracle as oracle  # noqa: E402
+from paper_2504_19442_b200 import (  # noqa: E402
+    ArgumentError,
+    CollectiveFault,
+    ProblemShape,
+    TileSchedule,
+    TileStep,
+    WorldSpec,
+    ag_gemm,
+    ag_order_switch,
+    gemm_rs,
+    init_world,
+    make_ag_gemm_buffers,
+    make_gemm_rs_buffers,
+    rs_inter_order,
+)
+
+pytestmark = pytest.mark.gpu
+BF16 = torch.bfloat16
+
+
+@contextlib.contextmanager
+def make_world(world_size, heap_bytes=1 << 24, timeout_s=10.0):
+    w = init_world(WorldSpec(world_size=world_size, heap_bytes=heap_bytes, timeout_s=timeout_s))
+    try:
+        yield w
+    finally:
+        w.close()
+
+
+def to_np(x):
+    if isinstance(x, torch.Tensor):
+        return x.float().cpu().numpy()
+    if isinstance(x, (list, tuple)):
+        return type(x)(to_np(v) for v in x)
+    return x
+
+
+def run_np(world, body):
+    """Run ``body`` on every rank and convert the results afterwards: a rank
+    body must not block on a device->host copy while sibling ranks of the
+    same process still have to launch (the driver serialises pageable
+    copies, so the blocked copy would hold back a peer's launch)."""
+    return [to_np(r) for r in world.run(body)]
+
+
+def perm_schedule(rank, order):
+    return TileSchedule(rank, [TileStep(c, () if c == rank else (c,)) for c in order])
+
+
+def ints(rng, lo, hi, shape):
+    return rng.integers(lo, hi, shape).astype(np.int64)
+
+
+def dev(x, rank_pe):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(BF16).to(rank_pe.torch_device)
+
+
+def test_ag_gemm_identity_shards_give_back_b(rng):
+    shape = ProblemShape(m=256, n=64, k=256, dtype="bfloat16")
+    with make_world(2) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        eye = np.eye(256, dtype=np.int64)
+        shards = [eye[:128], eye[128:]]
+        b = ints(rng, -1, 2, (256, 64))
+
+        def body(pe):
+            out = ag_gemm(pe, dev(shards[pe.rank], pe), dev(b, pe), shape,
+                          ag_order_switch(pe.rank, 2), bufs)
+            return out
+
+        for out in run_np(w, body):
+            assert np.array_equal(out, b)
+
+
+@pytest.mark.parametrize("world_size", [1, 2, 4, 8])
+def test_ag_gemm_random_vs_dense_oracle(rng, world_size):
+    shape = ProblemShape(m=256 * world_size, n=192, k=320, dtype="bfloat16")
+    rows = shape.m // world_size
+    with make_world(world_size) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (rows, shape.k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (shape.k, shape.n))
+        ref = oracle.ag_gemm_reference(shards, b)
+        assert np.abs(ref).max() < 256  # exact in bf16
+
+        def body(pe):
+            return ag_gemm(pe, dev(shards[pe.rank], pe), dev(b, pe), shape,
+                           ag_order_switch(pe.rank, world_size), bufs)
+
+        for r, out in enumerate(run_np(w, body)):
+            assert np.array_equal(out, ref)
+            # bit-exact gathered layout: slot s = rank s's shard (collectives.py:95-97)
+            gathered = to_np(w.read_tensor(r, bufs.gathered, BF16, (shape.m, shape.k)))
+            assert np.array_equal(gathered, oracle.gathered_layout(shards))
+
+
+def test_ag_gemm_schedule_invariance(rng):
+    shape = ProblemShape(m=512, n=128, k=128, dtype="bfloat16")
+    with make_world(4) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (128, 128)) for _ in range(4)]
+        b = ints(rng, -1, 2, (128, 128))
+        ref = oracle.ag_gemm_reference(shards, b)
+        orders = [
+            lambda pe: ag_order_switch(pe.rank, 4),
+            lambda pe: rs_inter_order(pe.ctx, 1, 4),
+            lambda pe: perm_schedule(pe.rank, [3, 1, 0, 2]),
+            lambda pe: perm_schedule(pe.rank, list(reversed(range(4)))),
+        ]
+        for make_sched in orders:
+            def body(pe):
+                return ag_gemm(pe, dev(shards[pe.rank], pe), dev(b, pe), shape, make_sched(pe),
+                               bufs)
+
+            for out in run_np(w, body):
+                assert np.array_equal(out, ref)
+
+
+def test_ag_gemm_back_to_back_without_reset(rng):
+    # epochs make consecutive calls safe with no reset or join in between
+    shape = ProblemShape(m=512, n=256, k=256, dtype="bfloat16")
+    with make_world(4) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        rounds = 5
+        shards = [[ints(rng, -1, 2, (128, 256)) for _ in range(4)] for _ in range(rounds)]
+        b = ints(rng, -1, 2, (256, 256))
+
+        def body(pe):
+            bb = dev(b, pe)
+            xs = [dev(shards[i][pe.rank], pe) for i in range(rounds)]  # stage first
+            outs = [ag_gemm(pe, xs[i], bb, shape, ag_order_switch(pe.rank, 4), bufs, reset=False)
+                    for i in range(rounds)]
+            return outs
+
+        for outs in run_np(w, body):
+            for i, out in enumerate(outs):
+                assert np.array_equal(out, oracle.ag_gemm_reference(shards[i], b))
+
+
+def test_ag_gemm_flags_zero_after_reset(rng):
+    shape = ProblemShape(m=256, n=64, k=64, dtype="bfloat16")
+    with make_world(2) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (128, 64)) for _ in range(2)]
+        b = ints(rng, -1, 2, (64, 64))
+        run_np(w, lambda pe: ag_gemm(pe, dev(shards[pe.rank], pe), dev(b, pe), shape,
+                                 ag_order_switch(pe.rank, 2), bufs))
+        assert w.sweep_signals() == {}
+
+
+def test_ag_gemm_wait_counts_and_no_barriers(rng):
+    shape = ProblemShape(m=512, n=64, k=64, dtype="bfloat16")
+    with make_world(4) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (128, 64)) for _ in range(4)]
+        b = ints(rng, -1, 2, (64, 64))
+        w.reset_counters()
+        run_np(w, lambda pe: ag_gemm(pe, dev(shards[pe.rank], pe), dev(b, pe), shape,
+                                 ag_order_switch(pe.rank, 4), bufs))
+        for r in range(4):
+            c = w.counters(r)
+            assert c.get("wait", 0) == 3
+            assert c.get("barrier_all", 0) == 0
+
+
+def test_ag_gemm_shape_mismatch():
+    shape = ProblemShape(m=256, n=64, k=64, dtype="bfloat16")
+    with make_world(2) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+
+        def body(pe):
+            bad = torch.zeros((3, 64), dtype=BF16, device=pe.torch_device)
+            b = torch.zeros((64, 64), dtype=BF16, device=pe.torch_device)
+            return ag_gemm(pe, bad, b, shape, ag_order_switch(pe.rank, 2), bufs)
+
+        with pytest.raises(CollectiveFault) as info:
+            run_np(w, body)
+        assert isinstance(info.value.first, ArgumentError)
+
+
+def test_ag_gemm_non_covering_schedule_rejected():
+    shape = ProblemShape(m=256, n=64, k=64, dtype="bfloat16")
+    with make_world(2) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+
+        def body(pe):
+            a = torch.zeros((128, 64), dtype=BF16, device=pe.torch_device)
+            b = torch.zeros((64, 64), dtype=BF16, device=pe.torch_device)
+            return ag_gemm(pe, a, b, shape, perm_schedule(pe.rank, [0]), bufs)
+
+        with pytest.raises(CollectiveFault) as info:
+            run_np(w, body)
+        assert isinstance(info.value.first, ArgumentError)
+
+
+def test_gemm_rs_world_of_one_is_plain_matmul(rng):
+    shape = ProblemShape(m=256, n=128, k=192, dtype="bfloat16")
+    with make_world(1) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        a = ints(rng, -2, 3, (256, 192))
+        b = ints(rng, -1, 2, (192, 128))
+        out = run_np(w, lambda pe: gemm_rs(pe, dev(a, pe), dev(b, pe), shape,
+                                       rs_inter_order(pe.ctx, 1, 1), bufs))
+        assert np.array_equal(out[0], a @ b)
+
+
+def test_gemm_rs_all_ones_contribution_pattern():
+    shape = ProblemShape(m=256, n=64, k=64, dtype="bfloat16")
+    with make_world(2) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        a = np.ones((256, 64), dtype=np.int64)
+        b = np.eye(64, dtype=np.int64)
+        outs = run_np(w, lambda pe: gemm_rs(pe, dev(a, pe), dev(b, pe), shape,
+                                        rs_inter_order(pe.ctx, 1, 2), bufs))
+        for out in outs:
+            assert (out == 2).all()
+
+
+@pytest.mark.parametrize("world_size", [2, 4, 8])
+def test_gemm_rs_intra_random_vs_oracle(rng, world_size):
+    shape = ProblemShape(m=256 * world_size, n=192, k=128, dtype="bfloat16")
+    rows = shape.m // world_size
+    with make_world(world_size) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        amats = [ints(rng, -2, 3, (shape.m, shape.k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (shape.k, shape.n))
+        ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+        assert np.abs(ref).max() < 256
+
+        def body(pe):
+            return gemm_rs(pe, dev(amats[pe.rank], pe), dev(b, pe), shape,
+                           rs_inter_order(pe.ctx, 1, world_size), bufs)
+
+        for r, out in enumerate(run_np(w, body)):
+            assert np.array_equal(out, ref[r])
+            staging = to_np(w.read_tensor(r, bufs.staging, BF16, (world_size, rows, shape.n)))
+            # bit-exact scatter layout: slot s on rank r = rows r of A_s @ B_s
+            expect = oracle.staging_layout(amats, [b] * world_size, r)
+            assert np.array_equal(staging, expect)
+
+
+def test_gemm_rs_schedule_invariance_intra(rng):
+    shape = ProblemShape(m=1024, n=128, k=128, dtype="bfloat16")
+    with make_world(4) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        amats = [ints(rng, -2, 3, (1024, 128)) for _ in range(4)]
+        b = ints(rng, -1, 2, (128, 128))
+        ref = oracle.gemm_rs_reference(amats, [b] * 4)
+        for order in ([0, 1, 2, 3], [2, 0, 3, 1], [3, 2, 1, 0]):
+            outs = run_np(w, lambda pe: gemm_rs(pe, dev(amats[pe.rank], pe), dev(b, pe), shape,
+                                            perm_schedule(pe.rank, order),
+                                            bufs))
+            for r, out in enumerate(outs):
+                assert np.array_equal(out, ref[r])
+
+
+def test_gemm_rs_back_to_back_without_reset(rng):
+    shape = ProblemShape(m=1024, n=256, k=128, dtype="bfloat16")
+    with make_world(4) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        rounds = 4
+        amats = [[ints(rng, -2, 3, (1024, 128)) for _ in range(4)] for _ in range(rounds)]
+        b = ints(rng, -1, 2, (128, 256))
+
+        def body(pe):
+            bb = dev(b, pe)
+            xs = [dev(amats[i][pe.rank], pe) for i in range(rounds)]  # stage first
+            outs = [gemm_rs(pe, xs[i], bb, shape, rs_inter_order(pe.ctx, 1, 4), bufs, reset=False)
+                    for i in range(rounds)]
+            return outs
+
+        for r, outs in enumerate(run_np(w, body)):
+            for i, out in enumerate(outs):
+                assert np.array_equal(out, oracle.gemm_rs_reference(amats[i], [b] * 4)[r])
+
+
+def test_tp_mlp_float_tolerance():
+    # the Llama-MLP pattern at reduced size: X shard -> ag_gemm -> H -> gemm_rs -> Y shard,
+    # random normal bf16, rel Frobenius <= 1e-2 vs an fp32 reference (north star)
+    W, M, K, N = 4, 1024, 512, 768
+    g = np.random.default_rng(0)
+    xs = [g.standard_normal((M // W, K)).astype(np.float32) for _ in range(W)]
+    ups = [g.standard_normal((K, N // W)).astype(np.float32) * 0.05 for _ in range(W)]
+    downs = [g.standard_normal((N // W, K)).astype(np.float32) * 0.05 for _ in range(W)]
+    ag_shape = ProblemShape(m=M, n=N // W, k=K, dtype="bfloat16")
+    rs_shape = ProblemShape(m=M, n=K, k=N // W, dtype="bfloat16")
+    with make_world(W, heap_bytes=1 << 25) as w:
+        agb = make_ag_gemm_buffers(w, ag_shape)
+        rsb = make_gemm_rs_buffers(w, rs_shape)
+
+        def body(pe):
+            t = lambda x: torch.from_numpy(x).to(BF16).to(pe.torch_device)  # noqa: E731
+            x, up, down = t(xs[pe.rank]), t(ups[pe.rank]), t(downs[pe.rank])  # stage first
+            h = ag_gemm(pe, x, up, ag_shape, ag_order_switch(pe.rank, W), agb)
+            y = gemm_rs(pe, h, down, rs_shape, rs_inter_order(pe.ctx, 1, W), rsb)
+            return h, y
+
+        res = run_np(w, body)
+    xb = [torch.from_numpy(x).to(BF16).float().numpy() for x in xs]
+    ub = [torch.from_numpy(x).to(BF16).float().numpy() for x in ups]
+    db = [torch.from_numpy(x).to(BF16).float().numpy() for x in downs]
+    x_full = np.vstack(xb)
+    hs = [x_full @ ub[r] for r in range(W)]
+    y_full = sum(torch.from_numpy(hs[r]).to(BF16).float().numpy() @ db[r] for r in range(W))
+    for r, (h, y) in enumerate(res):
+        assert np.linalg.norm(h - hs[r]) / np.linalg.norm(hs[r]) < 1e-2
+        rows = M // W
+        ref = y_full[r * rows:(r + 1) * rows]
+        assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-2
