@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: the tensor-parallel MLP pair
+
+    X shard --ag_gemm--> H --gemm_rs--> Y shard
+
+on the Llama-3-70B MLP per-rank shapes of BASELINE.json (C3: AG+GEMM
+ProblemShape(m=8192, n=28672/8=3584, k=8192); C4: GEMM+RS ProblemShape(m=8192,
+n=8192, k=28672/8=3584)), bf16, synthetic data.  Weak scaling: every rank
+runs that per-rank pair at TP=N (N=1: no peers, the gathers/scatters are local).
+
+    python bench.py [--gpus N --steps K --warmup W]            (torchrun for N>1)
+    python bench.py --impl reference ...                       (CPU oracle arm)
+
+Prints ONE JSON line on rank 0.  `value` = whole-job TFLOPS (all ranks'
+algorithmic FLOPs / max-over-ranks device time); `e2e` = the same through the
+public API with host buffers (pinned H2D of X, D2H of Y inside the timed
+region); `roofline` = the dominant kernel (the fused AG+GEMM call) against the
+measured dense-bf16 peak; `cpu_baseline` = the numpy oracle port on the host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("AG+GEMM / GEMM+RS TFLOPS/GPU & % roofline at TP=1/2/4/8 vs unfused cuBLAS+NCCL")
+AG = dict(m=8192, n=3584, k=8192)   # C3 per-rank ProblemShape
+RS = dict(m=8192, n=8192, k=3584)   # C4 per-rank ProblemShape
+FALLBACK_PEAK_TFLOPS = 1590.0       # B200_PROFILING.md fallback (burst)
+
+
+def flops(shape):
+    return 2.0 * shape["m"] * shape["n"] * shape["k"]
+
+
+STEP_FLOPS = flops(AG) + flops(RS)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (capped at 50)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-unfused", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    except Exception:  # noqa: BLE001
+        return FALLBACK_PEAK_TFLOPS, "fallback (B200_PROFILING.md 1.59 PFLOP/s)"
+
+
+def ncu_traffic():
+    """dram read+write bytes per launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        win = [p for t, p in self.samples if t0 - 0.1 <= t <= t1 + 0.1]
+        if not win:
+            win = [p for _, p in self.samples]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(p[0]) for p in win if p[0].replace(".", "").isdigit()]
+        mx = [float(p[1]) for p in win if p[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in win for i in range(4) if p[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(win)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline): the numpy port of the
+# reference's ag_gemm / gemm_rs (oracle/minishmem_oracle.py), fp32 BLAS on all
+# host cores, on a row sample of the per-rank shapes.
+
+def cpu_sample_step(rows_sample, rng_seed=0):
+    import numpy as np
+
+    from oracle import minishmem_oracle as oracle
+
+    g = np.random.default_rng(rng_seed)
+    x = g.standard_normal((rows_sample, AG["k"]), dtype=np.float32)
+    w_up = g.standard_normal((AG["k"], AG["n"]), dtype=np.float32)
+    w_dn = g.standard_normal((RS["k"], RS["n"]), dtype=np.float32)
+
+    def step():
+        (h,), _ = oracle.port_ag_gemm([x], [w_up], [[0]])
+        (y,), _ = oracle.port_gemm_rs([h], [w_dn], [[0]])
+        return y
+
+    return step, 2.0 * rows_sample * (AG["n"] * AG["k"] + RS["n"] * RS["k"])
+
+
+def cpu_measure(steps, warmup, budget_s=20.0):
+    """Calibrate the row sample so one step takes ~budget_s/steps, then time."""
+    rows = 128
+    step, fl = cpu_sample_step(rows)
+    t0 = time.perf_counter()
+    step()
+    dt = time.perf_counter() - t0
+    per_step_target = max(0.2, min(2.0, budget_s / max(1, steps)))
+    rows = int(max(128, min(AG["m"], rows * per_step_target / max(dt, 1e-3))) // 128 * 128)
+    step, fl = cpu_sample_step(rows)
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    cores = os.cpu_count()
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+    return {
+        "value": fl / dt / 1e12, "unit": "TFLOPS",
+        "cores": int(threads) if threads else cores, "kind": "port",
+        "sample": (f"oracle port (numpy fp32 BLAS) of ag_gemm+gemm_rs at W=1 on {rows} of "
+                   f"{AG['m']} rows of the C3/C4 per-rank shapes, {steps} steps, "
+                   f"{dt * 1e3:.1f} ms/step"),
+        "ms_per_step": dt * 1e3,
+    }
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 10))
+    warm = max(0, min(args.warmup, 1))
+    cb = cpu_measure(steps, warm, budget_s=30.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "TFLOPS",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": cb["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(world),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "TFLOPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": ("reference = numpy restatement of minishmem ag_gemm/gemm_rs (the reference "
+                 "package is pure Python+numpy and cannot travel to the GPU box)"),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(world):
+    return {
+        "workload": ("Llama-3-70B MLP TP pair per rank: ag_gemm ProblemShape(m=8192,n=3584,"
+                     "k=8192) -> gemm_rs ProblemShape(m=8192,n=8192,k=3584), bf16"),
+        "ag_shape": AG, "rs_shape": RS, "global_batch": AG["m"], "seq_len": None,
+        "parallelism": f"tp{world}",
+        "l2": "no flush: per-step working set ~0.55 GB > 126 MB L2",
+    }
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world_env != args.gpus:
+        args.gpus = world_env if world_env > 1 else args.gpus
+    if args.impl == "reference":
+        return run_reference(args, rank, args.gpus)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_19442_b200 as sb
+    from paper_2504_19442_b200 import _lib
+
+    torch.cuda.set_device(local)
+    N = world_env
+    heap = (AG["m"] * AG["k"] + RS["m"] * RS["n"]) * 2 + (64 << 20)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        world = sb.init_world_dist(heap_bytes=heap, timeout_s=30.0, device=local)
+    else:
+        world = sb.init_world(sb.WorldSpec(world_size=1, heap_bytes=heap, timeout_s=30.0,
+                                           devices=(local,)))
+    pe = world.pe(rank)
+    dev = pe.torch_device
+    ag_shape = sb.ProblemShape(dtype="bfloat16", **AG)
+    rs_shape = sb.ProblemShape(dtype="bfloat16", **RS)
+    agb = sb.make_ag_gemm_buffers(world, ag_shape)
+    rsb = sb.make_gemm_rs_buffers(world, rs_shape)
+    ag_sched = sb.ag_order_switch(rank, N)
+    rs_sched = sb.rs_inter_order(world.ranks[rank], 1, N)
+    rows = AG["m"] // N
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(rows, AG["k"], device=dev, generator=g).to(torch.bfloat16)
+    w_up = (torch.randn(AG["k"], AG["n"], device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    w_dn = (torch.randn(RS["k"], RS["n"], device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    stream = pe.stream()
+
+    def step(xin):
+        h = sb.ag_gemm(pe, xin, w_up, ag_shape, ag_sched, agb, reset=False)
+        return sb.gemm_rs(pe, h, w_dn, rs_shape, rs_sched, rsb, reset=False)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if N > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if N == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            step(x)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        t_wall0 = time.time()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(x)
+        ev1.record(stream)
+        barrier()
+        t_wall1 = time.time()
+        ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        # per-call split (the fused AG+GEMM call is the dominant kernel)
+        k2 = min(args.steps, 50)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(k2)]
+        for a, b, c in evs:
+            a.record(stream)
+            h = sb.ag_gemm(pe, x, w_up, ag_shape, ag_sched, agb, reset=False)
+            b.record(stream)
+            sb.gemm_rs(pe, h, w_dn, rs_shape, rs_sched, rsb, reset=False)
+            c.record(stream)
+        barrier()
+        ag_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b, _ in evs))
+        rs_ms = max_over_ranks(statistics.mean(b.elapsed_time(c) for _, b, c in evs))
+    clk = clocks.summary(t_wall0, t_wall1)
+
+    world.check_errors(rank)
+
+    # ------------------------------------------------------------------ e2e
+    k_e2e = args.e2e_steps or min(args.steps, 50)
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty((rows, RS["n"]), dtype=torch.bfloat16).pin_memory()
+    x_dev = [torch.empty_like(x) for _ in range(2)]
+    h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done_h2d = [torch.cuda.Event() for _ in range(2)]
+    done_use = [torch.cuda.Event() for _ in range(2)]
+    for i in range(k_e2e):
+        slot = i % 2
+        h2d.wait_event(e0)
+        if i >= 2:
+            h2d.wait_event(done_use[slot])
+        with torch.cuda.stream(h2d):
+            x_dev[slot].copy_(x_host, non_blocking=True)
+        done_h2d[slot].record(h2d)
+        stream.wait_event(done_h2d[slot])
+        with torch.cuda.stream(stream):
+            yd = step(x_dev[slot])
+        done_use[slot].record(stream)
+        d2h.wait_stream(stream)
+        with torch.cuda.stream(d2h):
+            y_host.copy_(yd, non_blocking=True)
+            yd.record_stream(d2h)
+    stream.wait_stream(d2h)
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / k_e2e)
+
+    # ------------------------------------------------------------- baselines
+    unfused = None
+    if not args.no_unfused:
+        with torch.cuda.stream(stream):
+            if N > 1:
+                xg = torch.empty((AG["m"], AG["k"]), dtype=torch.bfloat16, device=dev)
+                ys = torch.empty((rows, RS["n"]), dtype=torch.bfloat16, device=dev)
+
+                def ustep():
+                    dist.all_gather_into_tensor(xg, x)
+                    hh = torch.matmul(xg, w_up)
+                    yy = torch.matmul(hh, w_dn)
+                    dist.reduce_scatter_tensor(ys, yy)
+            else:
+                def ustep():
+                    hh = torch.matmul(x, w_up)
+                    torch.matmul(hh, w_dn)
+            for _ in range(3):
+                ustep()
+            barrier()
+            u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            u0.record(stream)
+            ku = min(args.steps, 50)
+            for _ in range(ku):
+                ustep()
+            u1.record(stream)
+            barrier()
+            ums = max_over_ranks(u0.elapsed_time(u1) / ku)
+        unfused = {"impl": "torch.matmul (cuBLASLt)" + (" + NCCL all_gather/reduce_scatter"
+                                                        if N > 1 else ""),
+                   "value": STEP_FLOPS * N / (ums * 1e-3) / 1e12, "unit": "TFLOPS",
+                   "ms_per_step": ums}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        cb = cpu_measure(steps=5, warmup=1, budget_s=15.0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    # ------------------------------------------------------------- roofline
+    peak, peak_src = peaks()
+    dom_ms = ag_ms
+    achieved = flops(AG) / (dom_ms * 1e-3) / 1e12
+    traffic = ncu_traffic().get("ag_gemm_kernel_dram_bytes")
+    bn = (ctypes_query_tile(_lib, rows, N, AG["n"]))
+    line = {
+        "metric": METRIC,
+        "value": STEP_FLOPS * N / (ms * 1e-3) / 1e12,
+        "unit": "TFLOPS",
+        "n_gpus": N, "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (random normal, seeded)",
+        "config": workload_config(N),
+        "tflops_per_gpu": STEP_FLOPS / (ms * 1e-3) / 1e12,
+        "breakdown": {"ag_gemm_ms": ag_ms, "gemm_rs_ms": rs_ms,
+                      "ag_gemm_tflops": flops(AG) / (ag_ms * 1e-3) / 1e12,
+                      "gemm_rs_tflops": flops(RS) / (rs_ms * 1e-3) / 1e12,
+                      "tile": bn},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "gemm_tp_kernel<MODE_AG> (fused ag_gemm call, CUDA events)",
+                     "per_launch_flops": flops(AG), "peak_source": peak_src},
+        "e2e": {"value": STEP_FLOPS * N / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+                "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": rows * RS["n"] * 2,
+                "ms_per_step": e2e_ms,
+                "how": "pinned X H2D + ag_gemm + gemm_rs + Y D2H per step, double-buffered"},
+        "unfused_baseline": unfused,
+        "cpu_baseline": cpu,
+        "gpu_launches": args.steps * 3,
+        "gpu_launches_note": "per step: AG GEMM kernel, RS GEMM kernel, RS reduction kernel",
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    clocks.stop()
+    world.close()
+    if N > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_query_tile(_lib, rows, world, n):
+    import ctypes
+
+    bn, cg, grid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.load().sh_query_tile_config(rows, world, n, ctypes.byref(bn), ctypes.byref(cg),
+                                     ctypes.byref(grid))
+    return {"bn": bn.value, "cta_group": cg.value, "grid": grid.value}
+
+
+if __name__ == "__main__":
+    main()

@@ -616,12 +616,9 @@ def init_world_dist(heap_bytes=1 << 30, signal_count=None, timeout_s=5.0, device
                      timeout_s=timeout_s)
     world = World(spec, _member=(rank, device))
 
-    def gather(b):
-        out = [None] * ws
-        dist.all_gather_object(out, b)
-        return out
+    from .dist import all_gather_bytes
 
     if ws > 1:
-        exchange_ipc_handles(world, gather)
+        exchange_ipc_handles(world, all_gather_bytes)
     dist.barrier()
     return world

@@ -137,7 +137,10 @@ Cfg choose_cfg(int rows, int world, int n, int sms) {
       // useful-work fraction (ragged edges compute padding) times wave fill,
       // with a small penalty for narrow tiles (more operand traffic per flop)
       double useful = double(rows) * n / (double(mblk) * bm * nblk * bn);
-      double score = eff * useful * (bn == 256 ? 1.0 : 0.94);
+      // measured on B200: a 256x128 pair tile runs at ~0.6x the per-flop rate
+      // of 256x256 (operand smem traffic per MMA doubles), so narrow tiles
+      // only win when they avoid a large amount of padding
+      double score = eff * useful * (bn == 256 ? 1.0 : 0.6);
       if (score > best_score) {
         best_score = score;
         best = Cfg{bn, cg, clusters * cg, mblk, nblk, tiles};
@@ -774,8 +777,9 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     if ((rc = store_flags(cs, &f, 1, epoch))) return rc;
   }
   // own slot (read by nobody during the call; the gemm reads a_shard directly)
-  CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
-                           cudaMemcpyDeviceToDevice, cs));
+  if (!env_int("SHB_SKIP_OWN_COPY", 0))
+    CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
+                             cudaMemcpyDeviceToDevice, cs));
 
   // ---- compute half on the caller's stream
   TensorMaps maps;

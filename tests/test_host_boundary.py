@@ -1,0 +1,111 @@
+"""Host logic and the C-ABI boundary, on CPU (no compute calls)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2504_19442_b200 import (AllocationError, ArgumentError, CollectiveFault,
+                                   ConfigurationError, ProblemShape, ShmemError,
+                                   SynchronizationFault, UsageError, WorldSpec, _lib)
+from paper_2504_19442_b200 import errors
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "shmem_b200.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(sh_\w+)\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(_lib.SIGNATURES)
+
+
+def test_library_loads_and_exports_every_symbol():
+    lib = _lib.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    assert lib.sh_version() >= 1
+    assert lib.sh_ipc_handle_size() == 64
+
+
+def test_argument_errors_without_gpu():
+    lib = _lib.load()
+    # argument validation precedes any CUDA work
+    rc = lib.sh_set_tile_config(96, 2)
+    assert rc == _lib.SH_ERR_ARG
+    with pytest.raises(ArgumentError, match="bn must be"):
+        _lib.check(rc)
+    assert lib.sh_set_tile_config(0, 0) == _lib.SH_OK
+    assert lib.sh_gemm(None, None, None, 0, 8, 8, 0, None) == _lib.SH_ERR_ARG
+    assert lib.sh_gemm(None, None, None, 8, 6, 8, 0, None) == _lib.SH_ERR_ARG  # n % 8
+    assert lib.sh_gemm(None, None, None, 8, 8, 8, 7, None) == _lib.SH_ERR_ARG  # dtype
+    lib.sh_gemm(None, None, None, 8, 6, 8, 0, None)
+    assert b"multiples of 8" in lib.sh_last_error()
+    out = ctypes.c_void_p()
+    assert lib.sh_world_create(0, None, 1 << 20, 0, 5.0, ctypes.byref(out)) == _lib.SH_ERR_CONFIG
+    assert lib.sh_world_create(2, None, 0, 0, 5.0, ctypes.byref(out)) == _lib.SH_ERR_CONFIG
+
+
+def test_status_codes_map_to_reference_taxonomy():
+    for code, exc in [(_lib.SH_ERR_ARG, ArgumentError), (_lib.SH_ERR_ALLOC, AllocationError),
+                      (_lib.SH_ERR_TIMEOUT, SynchronizationFault), (_lib.SH_ERR_STATE, UsageError),
+                      (_lib.SH_ERR_CONFIG, ConfigurationError)]:
+        with pytest.raises(exc):
+            _lib.check(code)
+    with pytest.raises(ShmemError):
+        _lib.check(_lib.SH_ERR_CUDA)
+    _lib.check(_lib.SH_OK)
+
+
+def test_error_hierarchy_matches_reference():
+    assert issubclass(errors.ArgumentError, ValueError)
+    assert issubclass(errors.RangeError, errors.ArgumentError)
+    cf = CollectiveFault("x", {2: ArgumentError("a"), 0: ArgumentError("b")})
+    assert isinstance(cf.first, ArgumentError) and set(cf.failures) == {0, 2}
+
+
+def test_problem_shape_validation():
+    with pytest.raises(ArgumentError):
+        ProblemShape(m=0, n=4, k=4)
+    with pytest.raises(ArgumentError):
+        ProblemShape(m=9, n=4, k=4).rows_per_rank(2)
+    with pytest.raises(ArgumentError):
+        ProblemShape(m=8, n=8, k=8, tile_m=-1)
+    assert ProblemShape(m=8, n=8, k=8).rows_per_rank(4) == 2
+    # the tensor-core path computes in bf16/fp16; int64 (the reference default)
+    # is rejected loudly instead of silently computed on the CPU
+    with pytest.raises(ArgumentError, match="bf16/fp16"):
+        ProblemShape(m=8, n=8, k=8).torch_dtype
+    import torch
+
+    assert ProblemShape(m=8, n=8, k=8, dtype="bf16").torch_dtype == torch.bfloat16
+    assert ProblemShape(m=8, n=8, k=8, dtype="float16").dtype_code == _lib.SH_DTYPE_FP16
+
+
+def test_world_spec_validation():
+    assert WorldSpec(world_size=4).signal_count == 64
+    assert WorldSpec(world_size=32).signal_count == 128
+    assert WorldSpec(world_size=4, n_nodes=2).local_world_size == 2
+    with pytest.raises(ConfigurationError):
+        WorldSpec(world_size=3, n_nodes=2)
+    with pytest.raises(ConfigurationError):
+        WorldSpec(world_size=4, signal_count=2)
+    with pytest.raises(ConfigurationError):
+        WorldSpec(world_size=2, devices=(0,))
+    with pytest.raises(ConfigurationError):
+        WorldSpec(world_size=2, heap_bytes=0)
+
+
+def test_world_refuses_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    from paper_2504_19442_b200 import init_world
+
+    with pytest.raises(ConfigurationError, match="no CUDA device"):
+        init_world(WorldSpec(world_size=1))
