@@ -44,6 +44,12 @@ struct TileParams {
   const uint64_t* ready;              // AG: my pad, ready[src] (written by src)
   uint64_t* rs_count[kMaxWorld];      // RS: &pad_d[reduction + rank]
   const uint64_t* rs_free;            // RS: my pad, producer[d] >= epoch-1: d reduced last call
+  const uint64_t* rs_mine;            // RS: my pad, reduction[s] (elements delivered by s)
+  uint64_t rs_target;                 // RS: epoch * rows * n, a chunk fully delivered
+  const uint16_t* staging_local;      // RS: my staging buffer (W slots of rows x n)
+  int fuse_reduce;                    // RS: reduce my chunk in the epilogue of its tiles
+  const uint16_t* own_src;            // AG: a_shard (rows x k)
+  uint16_t* own_dst;                  // AG: my gathered slot `rank` (rows x k), or null
   int* err;                           // host-mapped error word
   uint64_t timeout_ns;
 };
@@ -84,12 +90,18 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
   static_assert(BNC % 64 == 0, "per-CTA B tile must be a multiple of 64 columns");
   static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  // 227 KB of dynamic smem per CTA, minus alignment slack and barriers
   static constexpr int stages_for_smem() {
-    return (220 * 1024 - EPI_BYTES) / STAGE_BYTES;
+    return (227 * 1024 - 1024 - 256 - EPI_BYTES) / STAGE_BYTES;
   }
   static constexpr int STAGES = stages_for_smem() > 8 ? 8 : stages_for_smem();
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
+
+__device__ __forceinline__ float2 unpack2(uint32_t w, bool fp16) {
+  if (fp16) return __half22float2(*reinterpret_cast<const __half2*>(&w));
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+}
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi, bool fp16) {
   if (fp16) {
@@ -126,10 +138,8 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&maps.a_all);
     prefetch_tmap(&maps.b);
-    if (MODE == MODE_AG) {
-      prefetch_tmap(&maps.a_own);
-      prefetch_tmap(&maps.c);
-    }
+    prefetch_tmap(&maps.c);
+    if (MODE == MODE_AG) prefetch_tmap(&maps.a_own);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -230,23 +240,57 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = (warp - 2) * 32 + (int)lane;  // 0..127 within the epilogue group
     uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
     int buf = 0;
     int it = 0;
-    uint32_t freed = 0;  // RS: destinations observed free for this epoch
+    uint32_t freed = 0;    // RS: destinations observed free for this epoch
+    bool peers_in = false;  // RS fused: every peer's contribution to my chunk landed
+    const size_t slot_elems = (size_t)p.rows * p.n;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int chunk, mb, nb;
       decode_tile(p, t, chunk, mb, nb);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const int row = mb * (BM * CG) + (int)cta_rank * BM + q * 32;  // first row of slab
+      const int cta_row0 = mb * (BM * CG) + (int)cta_rank * BM;
+      const int row = cta_row0 + q * 32;  // first row of this warp's slab
       const int n0 = nb * BN;
+      if (MODE == MODE_AG && chunk == p.rank && p.own_dst != nullptr) {
+        // Own slot of the gather buffer (allgather_push_intra pushes to self
+        // too, collectives.py:95-97): idle epilogue warps copy this CTA's
+        // 128 rows x (k/nblk) slice of a_shard while the MMA runs.  The rows
+        // are hot in L2 (this tile's TMA reads them), so the copy costs HBM
+        // writes only and is spread evenly over the own chunk's tiles.
+        const int kv = p.k / 8;
+        const int v_lo = (int)((long long)nb * kv / p.nblk);
+        const int v_hi = (int)((long long)(nb + 1) * kv / p.nblk);
+        const int vpr = v_hi - v_lo;
+        const int nrows = max(0, min(BM, p.rows - cta_row0));
+        const uint4* src = reinterpret_cast<const uint4*>(p.own_src);
+        uint4* dst = reinterpret_cast<uint4*>(p.own_dst);
+        const int total = nrows * vpr;
+        for (int i = et; i < total; i += 128) {
+          const int r = i / vpr;
+          const size_t off = (size_t)(cta_row0 + r) * kv + v_lo + (i - r * vpr);
+          __stcs(dst + off, __ldg(src + off));
+        }
+      }
+      const bool fused_own = (MODE == MODE_RS) && p.fuse_reduce && chunk == p.rank;
       if (MODE == MODE_RS && !((freed >> chunk) & 1u)) {
         // dest must have reduced the previous call before its slot is reused
         if (lane == 0 && p.epoch > 1)
           spin_geq(p.rs_free + chunk, p.epoch - 1, p.err, p.timeout_ns, 2);
         __syncwarp();
         freed |= 1u << chunk;
+      }
+      if (fused_own && !peers_in) {
+        // the reduce side of rs_intra_streams (collectives.py:163-171) for my
+        // own chunk: every other source's rows must have landed; every lane
+        // acquires so its own loads below are ordered after the releases
+        for (int s = 0; s < p.world; ++s)
+          if (s != p.rank) spin_geq(p.rs_mine + s, p.rs_target, p.err, p.timeout_ns, 3);
+        __syncwarp();
+        peers_in = true;
       }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
@@ -265,28 +309,88 @@ __global__ void __launch_bounds__(192, 1)
             else mbar_arrive(&tempty[as]);
           }
         }
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        uint8_t* sb = stg + buf * 4096;
-        uint8_t* rowp = sb + lane * 128;
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t* src = (c < 4) ? &v0[c * 8] : &v1[(c - 4) * 8];
-          uint4 w;
-          w.x = pack2(__uint_as_float(src[0]), __uint_as_float(src[1]), FP16);
-          w.y = pack2(__uint_as_float(src[2]), __uint_as_float(src[3]), FP16);
-          w.z = pack2(__uint_as_float(src[4]), __uint_as_float(src[5]), FP16);
-          w.w = pack2(__uint_as_float(src[6]), __uint_as_float(src[7]), FP16);
-          *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) = w;
+        for (int e = 0; e < 16; ++e) {
+          pk[e] = pack2(__uint_as_float(v0[2 * e]), __uint_as_float(v0[2 * e + 1]), FP16);
+          pk[16 + e] = pack2(__uint_as_float(v1[2 * e]), __uint_as_float(v1[2 * e + 1]), FP16);
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (MODE == MODE_AG) tma_store_3d(&maps.c, sb, n0 + j * 64, row, chunk);
-          else tma_store_2d(&maps.out[chunk], sb, n0 + j * 64, row);
-          bulk_commit();
+        const int xcol = n0 + j * 64;
+        if (!fused_own) {
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint8_t* sb = stg + buf * 4096;
+          uint8_t* rowp = sb + lane * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) =
+                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (MODE == MODE_AG) tma_store_3d(&maps.c, sb, xcol, row, chunk);
+            else tma_store_2d(&maps.out[chunk], sb, xcol, row);
+            bulk_commit();
+          }
+          buf ^= 1;
+        } else {
+          // fused reduction of my own chunk: out = sum_{s ascending} slot_s in
+          // fp32 with slot_rank = this tile rounded to bf16 -- the exact
+          // arithmetic of the separate reduction kernel (and of the reference's
+          // ascending `acc +=`), minus one HBM round trip of every slot.
+          float acc[64];
+#pragma unroll
+          for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+          const int grow = row + (int)lane;
+          const bool row_ok = grow < p.rows;
+          for (int s = 0; s < p.world; ++s) {
+            if (s == p.rank) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                float2 f = unpack2(pk[e], FP16);
+                acc[2 * e] += f.x;
+                acc[2 * e + 1] += f.y;
+              }
+            } else if (row_ok) {
+              const uint4* src = reinterpret_cast<const uint4*>(
+                  p.staging_local + (size_t)s * slot_elems + (size_t)grow * p.n + xcol);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                if (xcol + c * 8 < p.n) {
+                  uint4 w = src[c];
+                  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    float2 f = unpack2(wv[e], FP16);
+                    acc[c * 8 + 2 * e] += f.x;
+                    acc[c * 8 + 2 * e + 1] += f.y;
+                  }
+                }
+              }
+            }
+          }
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          uint8_t* own_b = stg;
+          uint8_t* sum_b = stg + 4096;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int so = lane * 128 + ((c ^ (lane & 7)) << 4);
+            *reinterpret_cast<uint4*>(own_b + so) =
+                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            *reinterpret_cast<uint4*>(sum_b + so) = make_uint4(
+                pack2(acc[8 * c + 0], acc[8 * c + 1], FP16), pack2(acc[8 * c + 2], acc[8 * c + 3], FP16),
+                pack2(acc[8 * c + 4], acc[8 * c + 5], FP16), pack2(acc[8 * c + 6], acc[8 * c + 7], FP16));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&maps.out[chunk], own_b, xcol, row);  // staging slot `rank` (layout)
+            tma_store_3d(&maps.c, sum_b, xcol, row, 0);        // the reduced output rows
+            bulk_commit();
+          }
+          buf = 0;
         }
-        buf ^= 1;
       }
       if constexpr (MODE == MODE_RS) {
         if (lane == 0) {

@@ -11,6 +11,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -113,7 +114,10 @@ struct Cfg {
   int bn, cg, grid, mblk, nblk, tiles;
 };
 
-Cfg choose_cfg(int rows, int world, int n, int sms) {
+Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
+  // ranks sharing one GPU split its SMs, so that all their persistent GEMMs
+  // are co-resident (their epilogues wait on each other's stores)
+  if (share > 1) sms = std::max(2, (sms / share) & ~1);
   int cgs[2] = {2, 1};
   int bns[2] = {256, 128};
   Cfg best{};
@@ -311,6 +315,7 @@ struct RankState {
   int* err_host = nullptr;
   int* err_dev = nullptr;
   bool shares_gpu = false;  // another rank of this process uses the same device
+  int ranks_on_device = 1;  // ranks of this process on `device` (incl. this one)
 };
 
 struct sh_world {
@@ -470,7 +475,10 @@ int sh_world_create(int world_size, const int* devices, size_t heap_bytes, int s
     }
   for (int r = 0; r < world_size; ++r) {
     for (int q = 0; q < world_size; ++q)
-      if (q != r && w->r[q].device == w->r[r].device) w->r[r].shares_gpu = true;
+      if (q != r && w->r[q].device == w->r[r].device) {
+        w->r[r].shares_gpu = true;
+        w->r[r].ranks_on_device++;
+      }
     CUDA_TRY(cudaSetDevice(w->r[r].device));
     CUDA_TRY(cudaDeviceSynchronize());
   }
@@ -748,7 +756,8 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = rs->device;
-  Cfg cfg = choose_cfg(rows, W, n, num_sms(dev));
+  Cfg cfg = choose_cfg(rows, W, n, num_sms(dev), rs->ranks_on_device);
+  const bool own_by_ce = env_int("SHB_OWN_COPY_CE", 0) != 0;
 
   // ---- comm half: push own shard into every rank's slot `rank`
   // (allgather_push_intra, collectives.py:95-97).  Copy engine, in the order
@@ -776,8 +785,9 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     uint64_t* f = sig_addr(w, *rs, p, ready_base + rank);
     if ((rc = store_flags(cs, &f, 1, epoch))) return rc;
   }
-  // own slot (read by nobody during the call; the gemm reads a_shard directly)
-  if (!env_int("SHB_SKIP_OWN_COPY", 0))
+  // own slot: written by the GEMM's idle epilogue warps from L2-hot rows
+  // (own_dst below); the copy-engine path stays available for A/B checks
+  if (own_by_ce)
     CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
                              cudaMemcpyDeviceToDevice, cs));
 
@@ -818,6 +828,9 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
+  p.own_src = static_cast<const uint16_t*>(a_shard);
+  p.own_dst = own_by_ce ? nullptr
+                        : reinterpret_cast<uint16_t*>(own_gathered + (size_t)rank * chunk_bytes);
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
   if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s))) return rc;
@@ -874,7 +887,8 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   }
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device));
+  Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device), rs->ranks_on_device);
+  const bool fuse = env_int("SHB_RS_UNFUSED", 0) == 0;
 
   TensorMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -888,6 +902,13 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
     uint64_t d[2] = {(uint64_t)n, (uint64_t)k}, st[1] = {(uint64_t)n * es};
     uint32_t bx[2] = {64, 64};
     if ((rc = make_map(&maps.b, dtype, b, 2, d, st, bx))) return rc;
+  }
+  {
+    // reduced output rows (written by the fused epilogue of my own chunk)
+    uint64_t d3[3] = {(uint64_t)n, (uint64_t)rows, 1},
+             s3[2] = {(uint64_t)n * es, (uint64_t)rows * n * es};
+    uint32_t bx3[3] = {64, 32, 1};
+    if ((rc = make_map(&maps.c, dtype, out, 3, d3, s3, bx3))) return rc;
   }
   for (int d = 0; d < W; ++d) {
     // rank d's staging slot `rank` (collectives.py:160: dst_off = rank*chunk_bytes)
@@ -911,15 +932,26 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   p.epoch = epoch;
   for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);
   p.rs_free = sig_addr(w, *rs, rank, producer_base);
-  p.err = rs->err_dev;
-  p.timeout_ns = w->timeout_ns;
-  if ((rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s))) return rc;
-
-  // reduction of my W staging slots in ascending source order
   const uint16_t* staging =
       reinterpret_cast<const uint16_t*>(static_cast<char*>(rs->peer[rank]) + staging_off);
   const size_t slot_elems = (size_t)rows * n;
   const uint64_t target = epoch * (uint64_t)slot_elems;
+  p.rs_mine = sig_addr(w, *rs, rank, reduction_base);
+  p.rs_target = target;
+  p.staging_local = staging;
+  p.fuse_reduce = fuse ? 1 : 0;
+  p.err = rs->err_dev;
+  p.timeout_ns = w->timeout_ns;
+  if ((rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s))) return rc;
+
+  // reduction of my W staging slots in ascending source order: fused into the
+  // epilogue of my own chunk's tiles (scheduled last, rs_inter_order), or a
+  // separate vectorised pass when SHB_RS_UNFUSED=1
+  if (fuse) {
+    uint64_t* fl[SH_MAX_WORLD];
+    for (int q = 0; q < W; ++q) fl[q] = sig_addr(w, *rs, q, producer_base + rank);
+    return store_flags(s, fl, W, epoch);
+  }
   int sms = num_sms(rs->device);
   size_t nvec = (slot_elems + 7) / 8;
   int grid = (int)std::min<size_t>((nvec + 255) / 256, (size_t)sms * 4);

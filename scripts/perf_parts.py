@@ -30,9 +30,12 @@ print("torch AG shape     %7.1f us" % bench(lambda: torch.matmul(x, wu)))
 print("torch RS shape     %7.1f us" % bench(lambda: torch.matmul(h, wd)))
 print("d2d copy 128MB     %7.1f us" % bench(lambda: dst.copy_(x)))
 print("ag_gemm W=1        %7.1f us" % bench(lambda: sb.ag_gemm(pe, x, wu, ags, sa, agb, reset=False)))
-os.environ["SHB_SKIP_OWN_COPY"] = "1"
-print("ag_gemm no copy    %7.1f us" % bench(lambda: sb.ag_gemm(pe, x, wu, ags, sa, agb, reset=False)))
-del os.environ["SHB_SKIP_OWN_COPY"]
+os.environ["SHB_OWN_COPY_CE"] = "1"
+print("ag_gemm CE copy    %7.1f us" % bench(lambda: sb.ag_gemm(pe, x, wu, ags, sa, agb, reset=False)))
+del os.environ["SHB_OWN_COPY_CE"]
+os.environ["SHB_RS_UNFUSED"] = "1"
+print("gemm_rs unfused    %7.1f us" % bench(lambda: sb.gemm_rs(pe, h, wd, rss, sr, rsb, reset=False)))
+del os.environ["SHB_RS_UNFUSED"]
 print("gemm_rs W=1        %7.1f us" % bench(lambda: sb.gemm_rs(pe, h, wd, rss, sr, rsb, reset=False)))
 def step():
     hh = sb.ag_gemm(pe, x, wu, ags, sa, agb, reset=False)
