@@ -109,7 +109,8 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
 /* The GEMM core alone (TP=1, no symmetric heap): c(m,n) = a(m,k) @ b(k,n). */
 int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream);
 
-/* Tile override for tuning: bn in {0 (auto), 128, 256}; cta_group in {0 (auto), 1, 2}. */
+/* Tile override for tuning: bn in {0 (auto), 128, 224, 256}; cta_group in {0 (auto), 1, 2}
+ * (224 needs cta_group 2). */
 int sh_set_tile_config(int bn, int cta_group);
 /* Launch config chosen for a problem (for the bench's roofline bookkeeping). */
 int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid);

@@ -82,14 +82,19 @@ template <int BN, int CG>
 struct GemmCfg {
   static constexpr int BM = 128;  // rows per CTA (UMMA M per CTA)
   static constexpr int BK = 64;   // 128 bytes of bf16: one swizzle atom row
-  static constexpr int BNC = BN / CG;  // B columns staged per CTA
+  static constexpr int BNC = BN / CG;  // B columns the MMA reads per CTA
+  static constexpr int B_BOXES = (BNC + 63) / 64;  // 64-column TMA boxes staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BNC * BK * 2;
+  static constexpr int B_BYTES = B_BOXES * 64 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;
+  static constexpr int SUB = 32;                     // epilogue sub-tile: 32 columns
+  static constexpr int NSUB = BN / SUB;
+  static constexpr int EPI_BUF = 32 * SUB * 2;       // 32 rows x 64 B (SWIZZLE_64B)
+  static constexpr int EPI_NBUF = 4;                 // staging buffers per epilogue warp
+  static constexpr int EPI_BYTES = 4 * EPI_NBUF * EPI_BUF;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
-  static_assert(BNC % 64 == 0, "per-CTA B tile must be a multiple of 64 columns");
-  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  static_assert(BNC % 16 == 0 && BN % SUB == 0 && BN <= 256, "BN");
+  static_assert(CG == 2 || BN % 64 == 0, "1-CTA tiles stage whole 64-column boxes");
   // 227 KB of dynamic smem per CTA, minus alignment slack and barriers
   static constexpr int stages_for_smem() {
     return (227 * 1024 - 1024 - 256 - EPI_BYTES) / STAGE_BYTES;
@@ -189,14 +194,14 @@ __global__ void __launch_bounds__(192, 1)
             if (own) tma_load_2d(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
             else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
 #pragma unroll
-            for (int j = 0; j < BNC / 64; ++j)
+            for (int j = 0; j < C::B_BOXES; ++j)
               tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
                           kEvictNormal);
           } else {
             if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
             else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
 #pragma unroll
-            for (int j = 0; j < BNC / 64; ++j)
+            for (int j = 0; j < C::B_BOXES; ++j)
               tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
                                kEvictNormal);
           }
@@ -241,8 +246,9 @@ __global__ void __launch_bounds__(192, 1)
     // ===================== epilogue (warps 2..5) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = (warp - 2) * 32 + (int)lane;  // 0..127 within the epilogue group
-    uint8_t* stg = sEpi + (warp - 2) * 2 * 4096;
+    uint8_t* stg = sEpi + (warp - 2) * C::EPI_NBUF * C::EPI_BUF;
     int buf = 0;
+    bool paired = false;   // staging ring currently used as {own, sum} pairs
     int it = 0;
     uint32_t freed = 0;    // RS: destinations observed free for this epoch
     bool peers_in = false;  // RS fused: every peer's contribution to my chunk landed
@@ -295,13 +301,14 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      // 32-column sub-tiles: one tcgen05.ld (32 lanes x 32 fp32), bf16 pack,
+      // a 64-byte swizzled row per lane, one 32x32 TMA store
 #pragma unroll 1
-      for (int j = 0; j < BN / 64; ++j) {
-        uint32_t v0[32], v1[32];
-        tmem_ld_32x32b_x32(t_row + j * 64, v0);
-        tmem_ld_32x32b_x32(t_row + j * 64 + 32, v1);
+      for (int j = 0; j < C::NSUB; ++j) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + j * C::SUB, v);
         tmem_ld_wait();
-        if (j == BN / 64 - 1) {
+        if (j == C::NSUB - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -309,21 +316,26 @@ __global__ void __launch_bounds__(192, 1)
             else mbar_arrive(&tempty[as]);
           }
         }
-        uint32_t pk[32];
+        uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          pk[e] = pack2(__uint_as_float(v0[2 * e]), __uint_as_float(v0[2 * e + 1]), FP16);
-          pk[16 + e] = pack2(__uint_as_float(v1[2 * e]), __uint_as_float(v1[2 * e + 1]), FP16);
-        }
-        const int xcol = n0 + j * 64;
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]), FP16);
+        const int xcol = n0 + j * C::SUB;
+        const int swz = (lane >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk ^= row bits 1..2
         if (!fused_own) {
-          if (lane == 0) bulk_wait_read<1>();
+          // 4-deep ring of staging buffers: at most 3 stores still reading smem
+          // (drain fully when coming from the paired layout of fused tiles)
+          if (lane == 0) {
+            if (paired) bulk_wait_read<0>();
+            else bulk_wait_read<C::EPI_NBUF - 1>();
+          }
+          paired = false;
           __syncwarp();
-          uint8_t* sb = stg + buf * 4096;
-          uint8_t* rowp = sb + lane * 128;
+          uint8_t* sb = stg + buf * C::EPI_BUF;
+          uint8_t* rowp = sb + lane * 64;
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) =
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(rowp + ((c ^ swz) << 4)) =
                 make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
           fence_proxy_async_smem();
           __syncwarp();
@@ -332,21 +344,21 @@ __global__ void __launch_bounds__(192, 1)
             else tma_store_2d(&maps.out[chunk], sb, xcol, row);
             bulk_commit();
           }
-          buf ^= 1;
+          buf = (buf + 1) % C::EPI_NBUF;
         } else {
           // fused reduction of my own chunk: out = sum_{s ascending} slot_s in
           // fp32 with slot_rank = this tile rounded to bf16 -- the exact
           // arithmetic of the separate reduction kernel (and of the reference's
           // ascending `acc +=`), minus one HBM round trip of every slot.
-          float acc[64];
+          float acc[32];
 #pragma unroll
-          for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+          for (int e = 0; e < 32; ++e) acc[e] = 0.f;
           const int grow = row + (int)lane;
           const bool row_ok = grow < p.rows;
           for (int s = 0; s < p.world; ++s) {
             if (s == p.rank) {
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
+              for (int e = 0; e < 16; ++e) {
                 float2 f = unpack2(pk[e], FP16);
                 acc[2 * e] += f.x;
                 acc[2 * e + 1] += f.y;
@@ -355,7 +367,7 @@ __global__ void __launch_bounds__(192, 1)
               const uint4* src = reinterpret_cast<const uint4*>(
                   p.staging_local + (size_t)s * slot_elems + (size_t)grow * p.n + xcol);
 #pragma unroll
-              for (int c = 0; c < 8; ++c) {
+              for (int c = 0; c < 4; ++c) {
                 if (xcol + c * 8 < p.n) {
                   uint4 w = src[c];
                   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
@@ -369,13 +381,19 @@ __global__ void __launch_bounds__(192, 1)
               }
             }
           }
-          if (lane == 0) bulk_wait_read<0>();
+          // buffer pairs {0,1} / {2,3} alternate; one commit group per pair
+          if (lane == 0) {
+            if (paired) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
+          paired = true;
           __syncwarp();
-          uint8_t* own_b = stg;
-          uint8_t* sum_b = stg + 4096;
+          const int pair = (buf >> 1) & 1;
+          uint8_t* own_b = stg + (2 * pair) * C::EPI_BUF;
+          uint8_t* sum_b = stg + (2 * pair + 1) * C::EPI_BUF;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int so = lane * 128 + ((c ^ (lane & 7)) << 4);
+          for (int c = 0; c < 4; ++c) {
+            const int so = lane * 64 + ((c ^ swz) << 4);
             *reinterpret_cast<uint4*>(own_b + so) =
                 make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
             *reinterpret_cast<uint4*>(sum_b + so) = make_uint4(
@@ -389,7 +407,7 @@ __global__ void __launch_bounds__(192, 1)
             tma_store_3d(&maps.c, sum_b, xcol, row, 0);        // the reduced output rows
             bulk_commit();
           }
-          buf = 0;
+          buf = (pair ^ 1) * 2;
         }
       }
       if constexpr (MODE == MODE_RS) {

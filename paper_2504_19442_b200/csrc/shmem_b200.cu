@@ -114,22 +114,39 @@ struct Cfg {
   int bn, cg, grid, mblk, nblk, tiles;
 };
 
+// Raster group (m-blocks walked before moving to the next n-block).  If the
+// chunk's A rows fit in ~64 MB of L2 they all stay resident and B streams
+// through exactly once (group = every m-block); otherwise group as many
+// m-blocks as fit, so B is re-read ceil(mblk/group) times instead of once
+// per 8 m-blocks.  Less DRAM traffic = less power = higher clocks under the
+// 1 kW cap (measured: the GEMM runs power-limited).
+int raster_group(int rows, int k, int mblk, int bm) {
+  if (const char* e = getenv("SHB_GROUP_M")) return std::max(1, std::min(mblk, atoi(e)));
+  // B200's L2 behaves like ~2 x 63 MB (one partition per die) for data that
+  // every SM touches, so budget well under 63 MB for the resident A rows
+  const double budget = 32.0 * (1 << 20);
+  const double a_blk = (double)bm * k * 2;
+  if (a_blk * mblk <= budget) return std::max(1, mblk);
+  return std::max(1, std::min(mblk, (int)(budget / a_blk)));
+}
+
 Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
   // ranks sharing one GPU split its SMs, so that all their persistent GEMMs
   // are co-resident (their epilogues wait on each other's stores)
   if (share > 1) sms = std::max(2, (sms / share) & ~1);
   int cgs[2] = {2, 1};
-  int bns[2] = {256, 128};
+  int bns[3] = {256, 224, 128};
   Cfg best{};
   double best_score = -1;
   for (int ci = 0; ci < 2; ++ci) {
     int cg = cgs[ci];
     if (g_force_cg && g_force_cg != cg) continue;
     if (!g_force_cg && cg == 1) continue;  // pairs by default
-    for (int bi = 0; bi < 2; ++bi) {
+    for (int bi = 0; bi < 3; ++bi) {
       int bn = bns[bi];
       if (g_force_bn && g_force_bn != bn) continue;
       if (cg == 2 && bn < 128) continue;
+      if (cg == 1 && bn % 64) continue;
       int bm = 128 * cg;
       int mblk = (rows + bm - 1) / bm;
       int nblk = (n + bn - 1) / bn;
@@ -144,12 +161,17 @@ Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
       // measured on B200: a 256x128 pair tile runs at ~0.6x the per-flop rate
       // of 256x256 (operand smem traffic per MMA doubles), so narrow tiles
       // only win when they avoid a large amount of padding
-      double score = eff * useful * (bn == 256 ? 1.0 : 0.6);
+      double score = eff * useful * (bn == 256 ? 1.0 : bn == 224 ? 0.85 : 0.6);
       if (score > best_score) {
         best_score = score;
         best = Cfg{bn, cg, clusters * cg, mblk, nblk, tiles};
       }
     }
+  }
+  if (best_score < 0) {  // an override with no legal tile: use the default pair tile
+    int mblk = (rows + 255) / 256, nblk = (n + 255) / 256, tiles = world * mblk * nblk;
+    int clusters = std::min(tiles, sms / 2);
+    best = Cfg{256, 2, clusters * 2, mblk, nblk, tiles};
   }
   return best;
 }
@@ -158,7 +180,8 @@ Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
 // tensor maps
 
 int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_t* dims,
-             const uint64_t* strides_bytes, const uint32_t* box) {
+             const uint64_t* strides_bytes, const uint32_t* box,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   Driver& d = driver();
   if (!d.ok) return fail(SH_ERR_CUDA, "%s", d.why.c_str());
   cuuint64_t gd[3];
@@ -173,7 +196,7 @@ int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_
   CUresult r = d.encode(m, dtype == SH_DTYPE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                         rank, const_cast<void*>(ptr), gd, gs, bx, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(SH_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) ptr=%p dims=%llu,%llu", (int)r,
@@ -209,6 +232,7 @@ template <int MODE, bool FP16>
 int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaStream_t s) {
   if (c.cg == 2) {
     if (c.bn == 256) return launch_one<256, 2, MODE, FP16>(maps, p, c.grid, s);
+    if (c.bn == 224) return launch_one<224, 2, MODE, FP16>(maps, p, c.grid, s);
     return launch_one<128, 2, MODE, FP16>(maps, p, c.grid, s);
   }
   if (c.bn == 256) return launch_one<256, 1, MODE, FP16>(maps, p, c.grid, s);
@@ -240,6 +264,7 @@ template <int MODE, bool FP16>
 cudaError_t preload_mode() {
   cudaError_t e;
   if ((e = preload_one<256, 2, MODE, FP16>())) return e;
+  if ((e = preload_one<224, 2, MODE, FP16>())) return e;
   if ((e = preload_one<128, 2, MODE, FP16>())) return e;
   if ((e = preload_one<256, 1, MODE, FP16>())) return e;
   return preload_one<128, 1, MODE, FP16>();
@@ -651,7 +676,8 @@ int sh_clear_error(sh_world* w, int rank) {
 }
 
 int sh_set_tile_config(int bn, int cta_group) {
-  if (bn != 0 && bn != 128 && bn != 256) return fail(SH_ERR_ARG, "bn must be 0, 128 or 256");
+  if (bn != 0 && bn != 128 && bn != 224 && bn != 256)
+    return fail(SH_ERR_ARG, "bn must be 0, 128, 224 or 256");
   if (cta_group < 0 || cta_group > 2) return fail(SH_ERR_ARG, "cta_group must be 0, 1 or 2");
   g_force_bn = bn;
   g_force_cg = cta_group;
@@ -699,8 +725,8 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   }
   {
     uint64_t d3[3] = {(uint64_t)n, (uint64_t)m, 1}, s3[2] = {(uint64_t)n * es, (uint64_t)m * n * es};
-    uint32_t bx3[3] = {64, 32, 1};
-    if ((rc = make_map(&maps.c, dtype, c, 3, d3, s3, bx3))) return rc;
+    uint32_t bx3[3] = {32, 32, 1};
+    if ((rc = make_map(&maps.c, dtype, c, 3, d3, s3, bx3, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   }
   TileParams p;
   memset(&p, 0, sizeof(p));
@@ -712,7 +738,7 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = 8;
+  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
   p.order[0] = 0;
   p.epoch = 1;
   p.timeout_ns = 5000000000ull;
@@ -811,8 +837,8 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   {
     uint64_t d3[3] = {(uint64_t)n, (uint64_t)rows, (uint64_t)W},
              s3[2] = {(uint64_t)n * es, (uint64_t)rows * n * es};
-    uint32_t bx3[3] = {64, 32, 1};
-    if ((rc = make_map(&maps.c, dtype, c, 3, d3, s3, bx3))) return rc;
+    uint32_t bx3[3] = {32, 32, 1};
+    if ((rc = make_map(&maps.c, dtype, c, 3, d3, s3, bx3, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   }
   TileParams p;
   memset(&p, 0, sizeof(p));
@@ -824,7 +850,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = 8;
+  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
@@ -907,15 +933,16 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
     // reduced output rows (written by the fused epilogue of my own chunk)
     uint64_t d3[3] = {(uint64_t)n, (uint64_t)rows, 1},
              s3[2] = {(uint64_t)n * es, (uint64_t)rows * n * es};
-    uint32_t bx3[3] = {64, 32, 1};
-    if ((rc = make_map(&maps.c, dtype, out, 3, d3, s3, bx3))) return rc;
+    uint32_t bx3[3] = {32, 32, 1};
+    if ((rc = make_map(&maps.c, dtype, out, 3, d3, s3, bx3, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   }
   for (int d = 0; d < W; ++d) {
     // rank d's staging slot `rank` (collectives.py:160: dst_off = rank*chunk_bytes)
     char* dst = static_cast<char*>(rs->peer[d]) + staging_off + (size_t)rank * slot_bytes;
     uint64_t dd[2] = {(uint64_t)n, (uint64_t)rows}, st[1] = {(uint64_t)n * es};
-    uint32_t bx[2] = {64, 32};
-    if ((rc = make_map(&maps.out[d], dtype, dst, 2, dd, st, bx))) return rc;
+    uint32_t bx[2] = {32, 32};
+    if ((rc = make_map(&maps.out[d], dtype, dst, 2, dd, st, bx, CU_TENSOR_MAP_SWIZZLE_64B)))
+      return rc;
   }
   TileParams p;
   memset(&p, 0, sizeof(p));
@@ -927,7 +954,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = 8;
+  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);

@@ -23,7 +23,7 @@ def bench(fn, iters=50, warm=5):
 
 shapes = [(8192, 3584, 8192), (8192, 8192, 3584), (8192, 8192, 8192), (4096, 4096, 4096),
           (1024, 3584, 8192)]
-cfgs = [(0, 0), (256, 2), (128, 2)]
+cfgs = [(0, 0), (256, 2), (224, 2)]
 if len(sys.argv) > 1:
     cfgs = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]]
 for m, n, k in shapes:
