@@ -50,8 +50,62 @@ struct TileParams {
   int fuse_reduce;                    // RS: reduce my chunk in the epilogue of its tiles
   const uint16_t* own_src;            // AG: a_shard (rows x k)
   uint16_t* own_dst;                  // AG: my gathered slot `rank` (rows x k), or null
+  // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
+  // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
+  // clusters.  A cluster's range is walked backwards, so the partial head of a
+  // tile is produced first and the cluster finishing its tail (k_end = K)
+  // reduces the partials from the fp32 workspace.
+  int dp_tiles;
+  float* ws;                          // clusters x (CG*128) x BN fp32 partials
+  uint64_t* ws_flags;                 // clusters x CG x 4 epilogue warps
+  uint64_t ws_epoch;                  // launch counter of this workspace
   int* err;                           // host-mapped error word
   uint64_t timeout_ns;
+};
+
+struct WorkItem {
+  int t, kb0, kb1, kind;  // kind: 0 whole tile, 1 partial head (to workspace), 2 finishing tail
+};
+
+// Identical sequence of work items for the producer, MMA and epilogue roles.
+struct WorkIter {
+  int t, C, KB, dp;
+  long long u0, u, U;
+  __device__ __forceinline__ void init(const TileParams& p, int cid, int nclusters, int kb) {
+    C = nclusters;
+    KB = kb;
+    dp = p.dp_tiles;
+    t = cid;
+    U = (long long)(p.num_tiles - dp) * KB;
+    u0 = U * cid / C;
+    u = U * (cid + 1) / C;
+  }
+  __device__ __forceinline__ bool next(WorkItem& w) {
+    if (t < dp) {
+      w.t = t; w.kb0 = 0; w.kb1 = KB; w.kind = 0;
+      t += C;
+      return true;
+    }
+    if (u > u0) {
+      const long long tile = (u - 1) / KB;
+      const long long ts = tile * KB;
+      const long long sb = u0 > ts ? u0 : ts;
+      w.t = dp + (int)tile;
+      w.kb0 = (int)(sb - ts);
+      w.kb1 = (int)(u - ts);
+      w.kind = (w.kb0 == 0 && w.kb1 == KB) ? 0 : (w.kb1 == KB ? 2 : 1);
+      u = sb;
+      return true;
+    }
+    return false;
+  }
+  // first cluster whose range [U*i/C, U*(i+1)/C) contains stream-K unit v
+  __device__ __forceinline__ int owner(long long v) const {
+    int i = (int)(v * C / U);
+    while (i + 1 < C && U * (i + 1) / C <= v) ++i;
+    while (i > 0 && U * i / C > v) --i;
+    return i;
+  }
 };
 
 struct TensorMaps {
@@ -172,9 +226,12 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      WorkIter wi;
+      wi.init(p, cluster_id, num_clusters, num_kb);
+      WorkItem w;
+      while (wi.next(w)) {
         int chunk, mb, nb;
-        decode_tile(p, t, chunk, mb, nb);
+        decode_tile(p, w.t, chunk, mb, nb);
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
         const int col0 = nb * BN + (int)cta_rank * BNC;
         const bool own = (MODE == MODE_AG) && chunk == p.rank;
@@ -184,7 +241,7 @@ __global__ void __launch_bounds__(192, 1)
           fence_proxy_async_global();
           landed |= 1u << chunk;
         }
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
@@ -216,13 +273,16 @@ __global__ void __launch_bounds__(192, 1)
                                                 /*b MN-major*/ 1);
       uint32_t stage = 0, phase = 0;
       int it = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+      WorkIter wi;
+      wi.init(p, cluster_id, num_clusters, num_kb);
+      WorkItem w;
+      for (; wi.next(w); ++it) {
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait_cluster(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
@@ -234,7 +294,7 @@ __global__ void __launch_bounds__(192, 1)
             // B: MN-major SW128: 64-column atoms 8 KB apart (LBO), 8-row K
             // groups 1 KB apart (SBO); +2 KB per 16-row K step.
             const uint64_t bd = umma_desc(b_addr + kk * 2048, 64 * BK * 2, 1024, 2);
-            umma_f16<CG>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+            umma_f16<CG>(d_tmem, ad, bd, IDESC, (kb != w.kb0) || (kk != 0));
           }
           umma_commit<CG>(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -253,15 +313,18 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t freed = 0;    // RS: destinations observed free for this epoch
     bool peers_in = false;  // RS fused: every peer's contribution to my chunk landed
     const size_t slot_elems = (size_t)p.rows * p.n;
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+    WorkIter wi;
+    wi.init(p, cluster_id, num_clusters, num_kb);
+    WorkItem w;
+    for (; wi.next(w); ++it) {
       int chunk, mb, nb;
-      decode_tile(p, t, chunk, mb, nb);
+      decode_tile(p, w.t, chunk, mb, nb);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       const int cta_row0 = mb * (BM * CG) + (int)cta_rank * BM;
       const int row = cta_row0 + q * 32;  // first row of this warp's slab
       const int n0 = nb * BN;
-      if (MODE == MODE_AG && chunk == p.rank && p.own_dst != nullptr) {
+      if (MODE == MODE_AG && chunk == p.rank && p.own_dst != nullptr && w.kind != 1) {
         // Own slot of the gather buffer (allgather_push_intra pushes to self
         // too, collectives.py:95-97): idle epilogue warps copy this CTA's
         // 128 rows x (k/nblk) slice of a_shard while the MMA runs.  The rows
@@ -301,6 +364,44 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      const size_t ws_row_stride = (size_t)BN;
+      const int ws_row = (int)cta_rank * BM + q * 32 + (int)lane;  // row within the pair tile
+      if (w.kind == 1) {
+        // partial head of a stream-K tile: fp32 to this cluster's workspace
+        // slot, then a release flag per epilogue warp
+        float* dst = p.ws + ((size_t)cluster_id * (BM * CG) + ws_row) * ws_row_stride;
+#pragma unroll 1
+        for (int j = 0; j < C::NSUB; ++j) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + j * C::SUB, v);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(dst + j * C::SUB);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            d4[c] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                                __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+        }
+        tc_fence_before();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(&tempty[as], 0);
+          else mbar_arrive(&tempty[as]);
+          st_release_sys(p.ws_flags + ((size_t)cluster_id * CG + cta_rank) * 4 + q, p.ws_epoch);
+        }
+        __syncwarp();
+        continue;
+      }
+      int c_lo = 0, c_hi = -1;  // clusters holding this tile's earlier k-blocks
+      if (w.kind == 2) {
+        const long long ts = (long long)(w.t - p.dp_tiles) * num_kb;
+        c_lo = wi.owner(ts);
+        c_hi = wi.owner(ts + w.kb0 - 1);
+        for (int c = c_lo; c <= c_hi; ++c)
+          spin_geq(p.ws_flags + ((size_t)c * CG + cta_rank) * 4 + q, p.ws_epoch, p.err,
+                   p.timeout_ns, 5);
+        __syncwarp();
+      }
       // 32-column sub-tiles: one tcgen05.ld (32 lanes x 32 fp32), bf16 pack,
       // a 64-byte swizzled row per lane, one 32x32 TMA store
 #pragma unroll 1
@@ -308,6 +409,18 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + j * C::SUB, v);
         tmem_ld_wait();
+        for (int c = c_lo; c <= c_hi; ++c) {
+          const float4* s4 = reinterpret_cast<const float4*>(
+              p.ws + ((size_t)c * (BM * CG) + ws_row) * ws_row_stride + j * C::SUB);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float4 f = __ldcg(s4 + e);
+            v[4 * e] = __float_as_uint(__uint_as_float(v[4 * e]) + f.x);
+            v[4 * e + 1] = __float_as_uint(__uint_as_float(v[4 * e + 1]) + f.y);
+            v[4 * e + 2] = __float_as_uint(__uint_as_float(v[4 * e + 2]) + f.z);
+            v[4 * e + 3] = __float_as_uint(__uint_as_float(v[4 * e + 3]) + f.w);
+          }
+        }
         if (j == C::NSUB - 1) {
           tc_fence_before();
           __syncwarp();

@@ -16,6 +16,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -113,6 +114,51 @@ int num_sms(int dev) {
 struct Cfg {
   int bn, cg, grid, mblk, nblk, tiles;
 };
+
+// Stream-K tail: when the last wave of tiles would leave many CTA pairs idle,
+// the last full wave plus the partial one are split by k-block over all
+// clusters (the rest stays one-tile-per-cluster).  Returns dp_tiles.
+int stream_k_split(const Cfg& c, int num_kb) {
+  const int clusters = c.grid / c.cg;
+  const char* env = getenv("SHB_SK");
+  if (env && atoi(env) == 0) return c.tiles;
+  const int waves = (c.tiles + clusters - 1) / clusters;
+  const double eff = double(c.tiles) / double(waves * clusters);
+  const bool want = env ? atoi(env) != 0 : (eff < 0.92 && num_kb >= 8);
+  if (!want || c.tiles <= 0) return c.tiles;
+  const int full = c.tiles / clusters;
+  return full > 1 ? (full - 1) * clusters : 0;
+}
+
+// fp32 partial workspace for the stream-K tail of one stream of launches.
+struct SkWorkspace {
+  float* ws = nullptr;
+  uint64_t* flags = nullptr;
+  size_t ws_bytes = 0;
+  uint64_t epoch = 0;
+};
+
+int sk_reserve(SkWorkspace& w, int clusters, int cg, int bn) {
+  const size_t need = (size_t)clusters * cg * 128 * bn * sizeof(float);
+  const size_t nflags = (size_t)clusters * cg * 4;
+  if (w.ws && w.ws_bytes >= need) return SH_OK;
+  if (w.ws) {
+    cudaDeviceSynchronize();
+    cudaFree(w.ws);
+    cudaFree(w.flags);
+    w.ws = nullptr;
+  }
+  const size_t cap_clusters = 128;  // >= any B200 SM count / 2
+  const size_t bytes = std::max(need, cap_clusters * 2 * 128 * 256 * sizeof(float));
+  CUDA_TRY(cudaMalloc(&w.ws, bytes));
+  CUDA_TRY(cudaMalloc(&w.flags, cap_clusters * 2 * 4 * sizeof(uint64_t)));
+  CUDA_TRY(cudaMemset(w.flags, 0, cap_clusters * 2 * 4 * sizeof(uint64_t)));
+  CUDA_TRY(cudaDeviceSynchronize());
+  (void)nflags;
+  w.ws_bytes = bytes;
+  w.epoch = 0;
+  return SH_OK;
+}
 
 // Raster group (m-blocks walked before moving to the next n-block).  If the
 // chunk's A rows fit in ~64 MB of L2 they all stay resident and B streams
@@ -341,6 +387,7 @@ struct RankState {
   int* err_dev = nullptr;
   bool shares_gpu = false;  // another rank of this process uses the same device
   int ranks_on_device = 1;  // ranks of this process on `device` (incl. this one)
+  SkWorkspace sk;           // stream-K partials of this rank's AG launches
 };
 
 struct sh_world {
@@ -363,6 +410,7 @@ int init_rank_common(sh_world* w, RankState& rs) {
   int rc = ensure_preloaded(rs.device);
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(rs.device));
+  if ((rc = sk_reserve(rs.sk, num_sms(rs.device) / 2, 2, 256))) return rc;
   CUDA_TRY(cudaStreamCreateWithFlags(&rs.comm, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_in, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_done, cudaEventDisableTiming));
@@ -585,6 +633,8 @@ int sh_world_destroy(sh_world* w) {
     if (rs.ev_in) cudaEventDestroy(rs.ev_in);
     if (rs.ev_done) cudaEventDestroy(rs.ev_done);
     if (rs.err_host) cudaFreeHost(rs.err_host);
+    if (rs.sk.ws) cudaFree(rs.sk.ws);
+    if (rs.sk.flags) cudaFree(rs.sk.flags);
   }
   delete w;
   return SH_OK;
@@ -738,6 +788,17 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
+  p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
+  if (p.dp_tiles < p.num_tiles) {
+    static std::mutex mu;
+    static std::map<std::pair<int, void*>, SkWorkspace> pool;
+    std::lock_guard<std::mutex> g(mu);
+    SkWorkspace& ws = pool[{dev, stream}];
+    if ((rc = sk_reserve(ws, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
+    p.ws = ws.ws;
+    p.ws_flags = ws.flags;
+    p.ws_epoch = ++ws.epoch;
+  }
   p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
   p.order[0] = 0;
   p.epoch = 1;
@@ -854,6 +915,13 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
+  p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
+  if (p.dp_tiles < p.num_tiles) {
+    if ((rc = sk_reserve(rs->sk, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
+    p.ws = rs->sk.ws;
+    p.ws_flags = rs->sk.flags;
+    p.ws_epoch = ++rs->sk.epoch;
+  }
   p.own_src = static_cast<const uint16_t*>(a_shard);
   p.own_dst = own_by_ce ? nullptr
                         : reinterpret_cast<uint16_t*>(own_gathered + (size_t)rank * chunk_bytes);
@@ -963,6 +1031,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
       reinterpret_cast<const uint16_t*>(static_cast<char*>(rs->peer[rank]) + staging_off);
   const size_t slot_elems = (size_t)rows * n;
   const uint64_t target = epoch * (uint64_t)slot_elems;
+  p.dp_tiles = p.num_tiles;  // RS tiles publish per chunk; no stream-K split
   p.rs_mine = sig_addr(w, *rs, rank, reduction_base);
   p.rs_target = target;
   p.staging_local = staging;

@@ -23,7 +23,7 @@ def bench(fn, iters=50, warm=5):
 
 shapes = [(8192, 3584, 8192), (8192, 8192, 3584), (8192, 8192, 8192), (4096, 4096, 4096),
           (1024, 3584, 8192)]
-cfgs = [(0, 0), (256, 2), (224, 2)]
+cfgs = [(256, 2)]
 if len(sys.argv) > 1:
     cfgs = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]]
 for m, n, k in shapes:
@@ -34,8 +34,11 @@ for m, n, k in shapes:
     line = f"{m}x{n}x{k}: cublas {fl / t_ref / 1e9:7.1f} TF"
     for bn, cg in cfgs:
         _lib.check(_lib.load().sh_set_tile_config(bn, cg))
-        t = bench(lambda: sb.gemm(a, b))
-        line += f" | ours bn={bn} cg={cg} {fl / t / 1e9:7.1f} TF"
+        for sk in ("0", "1"):
+            os.environ["SHB_SK"] = sk
+            t = bench(lambda: sb.gemm(a, b))
+            line += f" | bn={bn} sk={sk} {fl / t / 1e9:7.1f}"
+        del os.environ["SHB_SK"]
     c = sb.gemm(a, b)
     ref = (a.float() @ b.float())
     err = ((c.float() - ref).norm() / ref.norm()).item()

@@ -324,3 +324,28 @@ def test_tp_mlp_float_tolerance():
         rows = M // W
         ref = y_full[r * rows:(r + 1) * rows]
         assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-2
+
+
+@pytest.mark.parametrize("world_size", [1, 2])
+def test_ag_gemm_stream_k_tail_exact(rng, monkeypatch, world_size):
+    # enough tiles for the stream-K tail (80 on 74 CTA pairs at W=1)
+    monkeypatch.setenv("SHB_SK", "1")
+    shape = ProblemShape(m=2560, n=2048, k=512, dtype="bfloat16")
+    rows = shape.m // world_size
+    with make_world(world_size, heap_bytes=1 << 26) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (rows, shape.k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (shape.k, shape.n))
+        ref = oracle.ag_gemm_reference(shards, b)
+        assert np.abs(ref).max() < 256
+
+        def body(pe):
+            x, bb = dev(shards[pe.rank], pe), dev(b, pe)
+            return [ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, world_size), bufs,
+                            reset=False) for _ in range(2)]
+
+        for r, outs in enumerate(run_np(w, body)):
+            for out in outs:
+                assert np.array_equal(out, ref)
+            gathered = to_np(w.read_tensor(r, bufs.gathered, BF16, (shape.m, shape.k)))
+            assert np.array_equal(gathered, oracle.gathered_layout(shards))
