@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(192, 1)
       const bool fused_own = (MODE == MODE_RS) && p.fuse_reduce && chunk == p.rank;
       if (MODE == MODE_RS && !((freed >> chunk) & 1u)) {
         // dest must have reduced the previous call before its slot is reused
-        if (lane == 0 && p.epoch > 1)
+        if (lane == 0 && p.epoch > 1 && chunk != p.rank)  // own slot: stream-ordered
           spin_geq(p.rs_free + chunk, p.epoch - 1, p.err, p.timeout_ns, 2);
         __syncwarp();
         freed |= 1u << chunk;

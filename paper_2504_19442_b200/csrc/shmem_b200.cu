@@ -856,8 +856,12 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   // side stream's copies could otherwise be queued behind another rank's
   // spinning GEMM on the same device (measured: 13/30 W=8 runs stalled).
   const bool push_on_main = rs->shares_gpu || env_int("SHB_PUSH_ON_MAIN", 0) != 0;
-  cudaStream_t cs = push_on_main ? s : rs->comm;
-  if (!push_on_main) {
+  // nothing to push (TP=1, own slot written by the GEMM): keep the side
+  // stream out of it entirely -- cross-stream event pairs measured to
+  // serialise the caller's pinned copies on other streams at TP=1
+  const bool use_comm = !push_on_main && (W > 1 || own_by_ce);
+  cudaStream_t cs = use_comm ? rs->comm : s;
+  if (use_comm) {
     CUDA_TRY(cudaEventRecord(rs->ev_in, s));
     CUDA_TRY(cudaStreamWaitEvent(rs->comm, rs->ev_in, 0));
   }
@@ -938,7 +942,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
       if (q != rank) fl[cnt++] = sig_addr(w, *rs, q, done_base + rank);
     if ((rc = store_flags(s, fl, cnt, epoch))) return rc;
   }
-  if (!push_on_main) {
+  if (use_comm) {
     CUDA_TRY(cudaEventRecord(rs->ev_done, rs->comm));
     CUDA_TRY(cudaStreamWaitEvent(s, rs->ev_done, 0));
   }
@@ -1043,11 +1047,14 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   // reduction of my W staging slots in ascending source order: fused into the
   // epilogue of my own chunk's tiles (scheduled last, rs_inter_order), or a
   // separate vectorised pass when SHB_RS_UNFUSED=1
-  if (fuse) {
-    uint64_t* fl[SH_MAX_WORLD];
-    for (int q = 0; q < W; ++q) fl[q] = sig_addr(w, *rs, q, producer_base + rank);
-    return store_flags(s, fl, W, epoch);
-  }
+  // publish "reduced epoch" to every peer: frees my staging slots for their
+  // next call (the join of collectives.py:1-10, made a flag).  My own slot is
+  // rewritten only by my own next call, stream-ordered, so no self flag.
+  uint64_t* fl[SH_MAX_WORLD];
+  int nfl = 0;
+  for (int q = 0; q < W; ++q)
+    if (q != rank) fl[nfl++] = sig_addr(w, *rs, q, producer_base + rank);
+  if (fuse) return store_flags(s, fl, nfl, epoch);
   int sms = num_sms(rs->device);
   size_t nvec = (slot_elems + 7) / 8;
   int grid = (int)std::min<size_t>((nvec + 255) / 256, (size_t)sms * 4);
@@ -1061,11 +1068,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
                                                  W, counters, target, rs->err_dev, w->timeout_ns);
   CUDA_TRY(cudaGetLastError());
 
-  // publish "reduced epoch" to every rank (incl. self): frees my staging
-  // slots for the next call (the join of collectives.py:1-10, made a flag)
-  uint64_t* fl[SH_MAX_WORLD];
-  for (int q = 0; q < W; ++q) fl[q] = sig_addr(w, *rs, q, producer_base + rank);
-  return store_flags(s, fl, W, epoch);
+  return store_flags(s, fl, nfl, epoch);
 }
 
 }  // extern "C"
