@@ -435,7 +435,10 @@ __global__ void __launch_bounds__(192, 1)
           pk[e] = pack2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]), FP16);
         const int xcol = n0 + j * C::SUB;
         const int swz = (lane >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk ^= row bits 1..2
-        if (!fused_own) {
+        // a world of one reduces a single slot: out == staging[0] bit for bit,
+        // so both stores are issued from one staging buffer
+        const bool dual = fused_own && p.world == 1;
+        if (!fused_own || dual) {
           // 4-deep ring of staging buffers: at most 3 stores still reading smem
           // (drain fully when coming from the paired layout of fused tiles)
           if (lane == 0) {
@@ -453,8 +456,12 @@ __global__ void __launch_bounds__(192, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (MODE == MODE_AG) tma_store_3d(&maps.c, sb, xcol, row, chunk);
-            else tma_store_2d(&maps.out[chunk], sb, xcol, row);
+            if constexpr (MODE == MODE_AG) {
+              tma_store_3d(&maps.c, sb, xcol, row, chunk);
+            } else {
+              tma_store_2d(&maps.out[chunk], sb, xcol, row);
+              if (dual) tma_store_3d(&maps.c, sb, xcol, row, 0);
+            }
             bulk_commit();
           }
           buf = (buf + 1) % C::EPI_NBUF;
