@@ -87,7 +87,7 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = path or LIB_PATH
+        p = path or os.environ.get("SHB_LIB") or LIB_PATH
         if not os.path.exists(p):
             raise ShmemError(
                 f"native library {p} not built; run `python -m paper_2504_19442_b200._build` "

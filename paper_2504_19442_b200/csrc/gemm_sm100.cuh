@@ -17,9 +17,9 @@
 // CTA owns 128 rows of A and BN/2 columns of B in shared memory and 128 x BN
 // fp32 accumulator columns in TMEM (double buffered across tiles).
 //
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
-// CTA) + TMEM allocator (both CTAs), warps 2..5 epilogue (TMEM -> regs ->
-// bf16 -> swizzled smem -> TMA store).
+// Warp roles (224 threads): warp 0 TMA producer, warp 1 MMA issuer (leader
+// CTA), warps 2..5 epilogue (TMEM -> regs -> bf16 -> swizzled smem -> TMA
+// store; warp 2 allocates TMEM), warp 6 own-slot copier (AG).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -48,8 +48,9 @@ struct TileParams {
   uint64_t rs_target;                 // RS: epoch * rows * n, a chunk fully delivered
   const uint16_t* staging_local;      // RS: my staging buffer (W slots of rows x n)
   int fuse_reduce;                    // RS: reduce my chunk in the epilogue of its tiles
-  const uint16_t* own_src;            // AG: a_shard (rows x k)
-  uint16_t* own_dst;                  // AG: my gathered slot `rank` (rows x k), or null
+  int copy_own;                       // AG: store own-chunk A stages into gathered[rank]
+  uint16_t* own_slot_ptr;             // AG: gathered[rank] (rows x k)
+  int dbg;                            // experiment switches (0 in production)
   // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
   // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
   // clusters.  A cluster's range is walked backwards, so the partial head of a
@@ -114,6 +115,7 @@ struct TensorMaps {
   CUtensorMap b;      // {n, k}
   CUtensorMap c;      // AG: C {n, rows, W}
   CUtensorMap out[kMaxWorld];  // RS: dest d's staging slot `rank`, {n, rows}
+  CUtensorMap own_slot;        // AG: my gather slot `rank`, {k, rows} (box = one A stage)
 };
 
 __device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chunk, int& mb,
@@ -151,10 +153,10 @@ struct GemmCfg {
   static_assert(CG == 2 || BN % 64 == 0, "1-CTA tiles stage whole 64-column boxes");
   // 227 KB of dynamic smem per CTA, minus alignment slack and barriers
   static constexpr int stages_for_smem() {
-    return (227 * 1024 - 1024 - 256 - EPI_BYTES) / STAGE_BYTES;
+    return (227 * 1024 - 1024 - 512 - EPI_BYTES) / STAGE_BYTES;
   }
   static constexpr int STAGES = stages_for_smem() > 8 ? 8 : stages_for_smem();
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 512;
 };
 
 __device__ __forceinline__ float2 unpack2(uint32_t w, bool fp16) {
@@ -171,8 +173,10 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi, bool fp16) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+constexpr int kThreads = 224;  // 7 warps: producer, MMA, 4 epilogue, own-slot copier
+
 template <int BN, int CG, int MODE, bool FP16>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_tp_kernel(const __grid_constant__ TensorMaps maps, const __grid_constant__ TileParams p) {
   using C = GemmCfg<BN, CG>;
   constexpr int BM = C::BM, BK = C::BK, BNC = C::BNC, STAGES = C::STAGES;
@@ -187,7 +191,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* stored_bar = tempty + 2;        // AG own copy: copier done with stage s
+  uint64_t* alanded_bar = stored_bar + STAGES;  // AG own copy: this CTA's A half landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(alanded_bar + STAGES);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -198,7 +204,10 @@ __global__ void __launch_bounds__(192, 1)
     prefetch_tmap(&maps.a_all);
     prefetch_tmap(&maps.b);
     prefetch_tmap(&maps.c);
-    if (MODE == MODE_AG) prefetch_tmap(&maps.a_own);
+    if (MODE == MODE_AG) {
+      prefetch_tmap(&maps.a_own);
+      if (p.copy_own) prefetch_tmap(&maps.own_slot);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -208,6 +217,10 @@ __global__ void __launch_bounds__(192, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG * 4);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&stored_bar[s], 1);
+      mbar_init(&alanded_bar[s], 1);
     }
     fence_mbarrier_init();
   }
@@ -223,54 +236,101 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
+    // The whole warp walks the loop (warp-uniform values stay in uniform
+    // registers); one elected lane issues the barrier/TMA instructions.
+    {
       uint32_t stage = 0, phase = 0;
       uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
+      uint32_t copy_mask = 0, stored_phase = 0;  // stages holding an own-slot copy
+      const uint64_t b_hint = (p.dbg & 8) ? kEvictLast : kEvictNormal;
       WorkIter wi;
       wi.init(p, cluster_id, num_clusters, num_kb);
       WorkItem w;
       while (wi.next(w)) {
         int chunk, mb, nb;
         decode_tile(p, w.t, chunk, mb, nb);
+        const bool own = (MODE == MODE_AG) && chunk == p.rank;
+        const bool copying = own && p.copy_own;
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
         const int col0 = nb * BN + (int)cta_rank * BNC;
-        const bool own = (MODE == MODE_AG) && chunk == p.rank;
         if (MODE == MODE_AG && !own && !((landed >> chunk) & 1u)) {
           // wait(ready[chunk]) of pipelines.py:130-141, as an acquire spin
-          spin_geq(p.ready + chunk, p.epoch, p.err, p.timeout_ns, 1);
-          fence_proxy_async_global();
+          if (lane == 0) {
+            spin_geq(p.ready + chunk, p.epoch, p.err, p.timeout_ns, 1);
+            fence_proxy_async_global();
+          }
+          __syncwarp();
           landed |= 1u << chunk;
         }
+        int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (((copy_mask >> stage) & 1u) && !(p.dbg & 2)) {
+            // the own-slot store of the previous occupant must have read it
+            mbar_wait(&stored_bar[stage], (stored_phase >> stage) & 1u);
+            stored_phase ^= 1u << stage;
+            copy_mask &= ~(1u << stage);
+          }
+          // k-block kb of n-block nb goes to the own slot iff kb == nb (mod nblk):
+          // each k-block of each m-block exactly once.  Its A half lands on a
+          // CTA-local barrier; the copier forwards the bytes to the leader's
+          // full barrier and keeps the stage until its store has read it.
+          bool copy_kb = false;
+          if (copying && !(p.dbg & 32)) {
+            copy_kb = cr == 0;
+            cr = (cr + 1 == p.nblk) ? 0 : cr + 1;
+            if (copy_kb) copy_mask |= 1u << stage;
+          }
           uint8_t* a_dst = sA + stage * C::A_BYTES;
           uint8_t* b_dst = sB + stage * C::B_BYTES;
-          if (leader) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
           const int kx = kb * BK;
-          if constexpr (CG == 1) {
-            if (own) tma_load_2d(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
-            else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+          if (elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
+            if (copy_kb) {
+              mbar_arrive_expect_tx(&alanded_bar[stage], C::A_BYTES);
+              tma_load_2d(&maps.a_own, &alanded_bar[stage], a_dst, kx, row0, kEvictNormal);
 #pragma unroll
-            for (int j = 0; j < C::B_BOXES; ++j)
-              tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
-                          kEvictNormal);
-          } else {
-            if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
-            else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+              for (int j = 0; j < C::B_BOXES; ++j) {
+                if constexpr (CG == 1)
+                  tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                              b_hint);
+                else
+                  tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64,
+                                   kx, b_hint);
+              }
+            } else if constexpr (CG == 1) {
+              if (own) tma_load_2d(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
+              else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
 #pragma unroll
-            for (int j = 0; j < C::B_BOXES; ++j)
-              tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
-                               kEvictNormal);
+              for (int j = 0; j < C::B_BOXES; ++j)
+                tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                            b_hint);
+            } else {
+              if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
+              else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+#pragma unroll
+              for (int j = 0; j < C::B_BOXES; ++j)
+                tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                                 b_hint);
+            }
           }
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    if (leader && lane == 0) {
+    // Warp-wide loop, one elected lane issues tcgen05.mma / commit.
+    // Descriptors are precomputed and advanced by plain adds:
+    //   A (K-major SW128): +32 B per 16-element K step -> +2 in addr>>4
+    //   B (MN-major SW128): +2 KB per 16-row K step   -> +128 in addr>>4
+    if (leader) {
       constexpr uint32_t IDESC = umma_idesc_f16(BM * CG, BN, FP16 ? 0 : 1, /*a K-major*/ 0,
                                                 /*b MN-major*/ 1);
+      const uint64_t a_desc0 = umma_desc(smem_u32(sA), 16, 1024, 2);
+      // B: 64-column atoms 8 KB apart (LBO), 8-row K groups 1 KB apart (SBO)
+      const uint64_t b_desc0 = umma_desc(smem_u32(sB), 64 * BK * 2, 1024, 2);
       uint32_t stage = 0, phase = 0;
       int it = 0;
       WorkIter wi;
@@ -285,33 +345,76 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+          const uint64_t ad = a_desc0 + (uint64_t)((stage * C::A_BYTES) >> 4);
+          const uint64_t bd = b_desc0 + (uint64_t)((stage * C::B_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            // A: K-major SW128, +32 B per 16-element K step.  SBO = 8 rows x 128 B.
-            const uint64_t ad = umma_desc(a_addr + kk * 32, 16, 1024, 2);
-            // B: MN-major SW128: 64-column atoms 8 KB apart (LBO), 8-row K
-            // groups 1 KB apart (SBO); +2 KB per 16-row K step.
-            const uint64_t bd = umma_desc(b_addr + kk * 2048, 64 * BK * 2, 1024, 2);
-            umma_f16<CG>(d_tmem, ad, bd, IDESC, (kb != w.kb0) || (kk != 0));
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_f16<CG>(d_tmem, ad + 2 * kk, bd + 128 * kk, IDESC,
+                           (kb != w.kb0) || (kk != 0));
+            umma_commit<CG>(&empty[stage]);
           }
-          umma_commit<CG>(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit<CG>(&tfull[as]);
+        if (elect_one()) umma_commit<CG>(&tfull[as]);
+        __syncwarp();
       }
+    }
+  } else if (warp == 6) {
+    // ===================== own-slot copier (AG) =====================
+    // Own slot of the gather buffer (allgather_push_intra pushes to self too,
+    // collectives.py:95-97): every A stage of the own chunk is already in
+    // smem for the MMA, so 1/nblk of them (k-block kb of n-block kb mod nblk
+    // -- each k-block of each m-block exactly once) are copied from smem into
+    // gathered[rank] once the MMAs consumed them.  No extra HBM or L2 reads.
+    if (MODE == MODE_AG && p.copy_own && lane == 0) {
+      uint32_t stage = 0, landed_phase = 0;
+      WorkIter wi;
+      wi.init(p, cluster_id, num_clusters, num_kb);
+      WorkItem w;
+      while (wi.next(w)) {
+        int chunk, mb, nb;
+        decode_tile(p, w.t, chunk, mb, nb);
+        const bool copying = chunk == p.rank && !(p.dbg & 32);
+        const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
+        int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          if (copying) {
+            if (cr == 0) {
+              // uses of a stage for copies alternate with `stored` acks, so
+              // this parity wait is never more than one phase away
+              mbar_wait(&alanded_bar[stage], (landed_phase >> stage) & 1u);
+              landed_phase ^= 1u << stage;
+              mbar_complete_tx_cluster(&full[stage], 0, C::A_BYTES);  // hand to the MMA
+              // evict-first: 1 B written per 2 B the GEMM keeps reading from
+              // L2; don't let the copy push the operands out
+              if (!(p.dbg & 16)) {
+                tma_store_2d_hint(&maps.own_slot, sA + stage * C::A_BYTES, kb * BK, row0,
+                                  (p.dbg & 4) ? kEvictNormal : kEvictFirst);
+                bulk_commit();
+                bulk_wait_read<0>();
+              }
+              mbar_arrive(&stored_bar[stage]);
+            }
+            cr = (cr + 1 == p.nblk) ? 0 : cr + 1;
+          }
+          if (++stage == STAGES) stage = 0;
+        }
+      }
+      bulk_wait<0>();
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int et = (warp - 2) * 32 + (int)lane;  // 0..127 within the epilogue group
     uint8_t* stg = sEpi + (warp - 2) * C::EPI_NBUF * C::EPI_BUF;
     int buf = 0;
     bool paired = false;   // staging ring currently used as {own, sum} pairs
     int it = 0;
     uint32_t freed = 0;    // RS: destinations observed free for this epoch
     bool peers_in = false;  // RS fused: every peer's contribution to my chunk landed
+    int pend_chunk = -1;    // RS: tile whose stores still have to be published
+    uint64_t pend_count = 0;
     const size_t slot_elems = (size_t)p.rows * p.n;
     WorkIter wi;
     wi.init(p, cluster_id, num_clusters, num_kb);
@@ -324,26 +427,6 @@ __global__ void __launch_bounds__(192, 1)
       const int cta_row0 = mb * (BM * CG) + (int)cta_rank * BM;
       const int row = cta_row0 + q * 32;  // first row of this warp's slab
       const int n0 = nb * BN;
-      if (MODE == MODE_AG && chunk == p.rank && p.own_dst != nullptr && w.kind != 1) {
-        // Own slot of the gather buffer (allgather_push_intra pushes to self
-        // too, collectives.py:95-97): idle epilogue warps copy this CTA's
-        // 128 rows x (k/nblk) slice of a_shard while the MMA runs.  The rows
-        // are hot in L2 (this tile's TMA reads them), so the copy costs HBM
-        // writes only and is spread evenly over the own chunk's tiles.
-        const int kv = p.k / 8;
-        const int v_lo = (int)((long long)nb * kv / p.nblk);
-        const int v_hi = (int)((long long)(nb + 1) * kv / p.nblk);
-        const int vpr = v_hi - v_lo;
-        const int nrows = max(0, min(BM, p.rows - cta_row0));
-        const uint4* src = reinterpret_cast<const uint4*>(p.own_src);
-        uint4* dst = reinterpret_cast<uint4*>(p.own_dst);
-        const int total = nrows * vpr;
-        for (int i = et; i < total; i += 128) {
-          const int r = i / vpr;
-          const size_t off = (size_t)(cta_row0 + r) * kv + v_lo + (i - r * vpr);
-          __stcs(dst + off, __ldg(src + off));
-        }
-      }
       const bool fused_own = (MODE == MODE_RS) && p.fuse_reduce && chunk == p.rank;
       if (MODE == MODE_RS && !((freed >> chunk) & 1u)) {
         // dest must have reduced the previous call before its slot is reused
@@ -351,6 +434,13 @@ __global__ void __launch_bounds__(192, 1)
           spin_geq(p.rs_free + chunk, p.epoch - 1, p.err, p.timeout_ns, 2);
         __syncwarp();
         freed |= 1u << chunk;
+      }
+      if (MODE == MODE_RS && fused_own && lane == 0 && pend_chunk >= 0) {
+        // publish before waiting on the peers: they may be waiting on it
+        bulk_wait<0>();
+        fence_proxy_async_global();
+        red_add_release_sys(p.rs_count[pend_chunk], pend_count);
+        pend_chunk = -1;
       }
       if (fused_own && !peers_in) {
         // the reduce side of rs_intra_streams (collectives.py:163-171) for my
@@ -531,20 +621,36 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       if constexpr (MODE == MODE_RS) {
+        // Publish the previous tile of a peer chunk now that this tile's
+        // stores are queued behind it (keeps the store-completion wait off
+        // the accumulator's critical path); my own fused chunk needs no
+        // counter -- its reduction happened right here.
         if (lane == 0) {
-          // count the elements this warp actually delivered (TMA clips the
-          // ragged edges), so a chunk is complete at exactly rows*n per call
-          const int vr = max(0, min(32, p.rows - row));
-          const int vc = max(0, min(BN, p.n - n0));
-          bulk_wait<0>();
-          fence_proxy_async_global();
-          fence_acq_rel_sys();
-          red_add_release_sys(p.rs_count[chunk], (uint64_t)vr * (uint64_t)vc);
+          if (pend_chunk >= 0) {
+            bulk_wait<C::NSUB>();
+            fence_proxy_async_global();
+            red_add_release_sys(p.rs_count[pend_chunk], pend_count);
+          }
+          pend_chunk = -1;
+          if (!fused_own) {
+            // count the elements this warp actually delivered (TMA clips the
+            // ragged edges), so a chunk is complete at exactly rows*n per call
+            const int vr = max(0, min(32, p.rows - row));
+            const int vc = max(0, min(BN, p.n - n0));
+            pend_chunk = chunk;
+            pend_count = (uint64_t)vr * (uint64_t)vc;
+          }
         }
         __syncwarp();
       }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) {
+      bulk_wait<0>();
+      if (MODE == MODE_RS && pend_chunk >= 0) {
+        fence_proxy_async_global();
+        red_add_release_sys(p.rs_count[pend_chunk], pend_count);
+      }
+    }
     __syncwarp();
   }
 

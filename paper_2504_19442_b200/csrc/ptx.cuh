@@ -79,6 +79,19 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
       : "memory");
 }
 
+// Decrement the pending transaction bytes of the barrier at the same smem
+// offset in cluster CTA `cta`, without an arrive.
+__device__ __forceinline__ void mbar_complete_tx_cluster(uint64_t* bar, uint32_t cta,
+                                                         uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.complete_tx.shared::cluster.relaxed.cluster.b64 [ra], %2;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "r"(cta), "r"(bytes)
+      : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -178,6 +191,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
                    m),
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, const void* src, int x,
+                                                  int y, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], "
+      "%4;" ::"l"(m),
+      "r"(smem_u32(src)), "r"(x), "r"(y), "l"(hint)
+      : "memory");
 }
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int x, int y,
@@ -360,9 +382,10 @@ __device__ __forceinline__ bool spin_geq(const uint64_t* flag, uint64_t target, 
   if (ld_acquire_sys(flag) >= target) return true;
   uint64_t t0 = globaltimer();
   uint32_t ns = 32;
-  while (true) {
+  for (uint32_t i = 1;; ++i) {
     if (ld_acquire_sys(flag) >= target) return true;
-    if (err && *reinterpret_cast<volatile int*>(err) != 0) return false;
+    // the error word is host memory (a PCIe round trip): poll it rarely
+    if ((i & 255) == 0 && err && *reinterpret_cast<volatile int*>(err) != 0) return false;
     if (globaltimer() - t0 > timeout_ns) {
       if (err) atomicCAS(err, 0, code);
       __threadfence_system();

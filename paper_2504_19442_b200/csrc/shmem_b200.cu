@@ -94,6 +94,11 @@ Driver& driver() {
   return d;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // ---------------------------------------------------------------------------
 // tile configuration
 
@@ -260,7 +265,7 @@ int launch_one(const TensorMaps& maps, const TileParams& p, int grid, cudaStream
   // smem attribute + carveout are set per device by preload_kernels()
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(192, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -288,6 +293,13 @@ int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaS
 template <int MODE>
 int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParams& p,
                 cudaStream_t s) {
+  if (env_int("SHB_TRACE", 0))
+    fprintf(stderr,
+            "[shb] mode=%d bn=%d cg=%d grid=%d rows=%d n=%d k=%d W=%d rank=%d mblk=%d nblk=%d "
+            "tiles=%d dp=%d group_m=%d epoch=%llu copy_own=%d fuse=%d err=%p ws=%p\n",
+            MODE, c.bn, c.cg, c.grid, p.rows, p.n, p.k, p.world, p.rank, p.mblk, p.nblk,
+            p.num_tiles, p.dp_tiles, p.group_m, (unsigned long long)p.epoch, p.copy_own,
+            p.fuse_reduce, (void*)p.err, (void*)p.ws);
   if (dtype == SH_DTYPE_FP16) return launch_mode<MODE, true>(c, maps, p, s);
   return launch_mode<MODE, false>(c, maps, p, s);
 }
@@ -441,10 +453,6 @@ inline uint64_t* sig_addr(sh_world* w, const RankState& rs, int peer, int sig) {
                                      8 * (size_t)sig);
 }
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
 
 int stream_wait_geq(RankState& rs, cudaStream_t s, const uint64_t* flag, uint64_t target,
                     uint64_t timeout_ns) {
@@ -926,9 +934,16 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     p.ws_flags = rs->sk.flags;
     p.ws_epoch = ++rs->sk.epoch;
   }
-  p.own_src = static_cast<const uint16_t*>(a_shard);
-  p.own_dst = own_by_ce ? nullptr
-                        : reinterpret_cast<uint16_t*>(own_gathered + (size_t)rank * chunk_bytes);
+  p.copy_own = own_by_ce ? 0 : 1;
+  p.dbg = env_int("SHB_DBG", 0);
+  p.own_slot_ptr = reinterpret_cast<uint16_t*>(own_gathered + (size_t)rank * chunk_bytes);
+  if (p.copy_own) {
+    uint64_t d[2] = {(uint64_t)k, (uint64_t)rows}, st[1] = {(uint64_t)k * es};
+    uint32_t bx[2] = {64, 128};
+    if ((rc = make_map(&maps.own_slot, dtype, own_gathered + (size_t)rank * chunk_bytes, 2, d, st,
+                       bx)))
+      return rc;
+  }
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
   if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s))) return rc;
