@@ -405,8 +405,9 @@ def main():
                 "how": "pinned X H2D + ag_gemm + gemm_rs + Y D2H per step, double-buffered"},
         "unfused_baseline": unfused,
         "cpu_baseline": cpu,
-        "gpu_launches": args.steps * 3,
-        "gpu_launches_note": "per step: AG GEMM kernel, RS GEMM kernel, RS reduction kernel",
+        "gpu_launches": args.steps * 2,
+        "gpu_launches_note": ("per step: gemm_tp_kernel<MODE_AG> + gemm_tp_kernel<MODE_RS> "
+                              "(RS reduction fused into the epilogue)"),
         "clocks": clk,
     }
     if rank == 0:
