@@ -232,11 +232,18 @@ def main():
     import paper_2504_19442_b200 as sb
     from paper_2504_19442_b200 import _lib
 
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     N = world_env
     heap = (AG["m"] * AG["k"] + RS["m"] * RS["n"]) * 2 + (64 << 20)
     if N > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # BENCH_BACKEND=gloo lets several ranks share one GPU (functional check
+        # of the N>1 path; NCCL refuses duplicate GPUs)
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         world = sb.init_world_dist(heap_bytes=heap, timeout_s=30.0, device=local)
     else:
         world = sb.init_world(sb.WorldSpec(world_size=1, heap_bytes=heap, timeout_s=30.0,
@@ -268,9 +275,9 @@ def main():
     def max_over_ranks(v):
         if N == 1:
             return v
-        t = torch.tensor([v], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        from paper_2504_19442_b200.dist import max_over_ranks as mor
+
+        return mor(v, device=dev if dist.get_backend() == "nccl" else None)
 
     clocks = Clocks(local)
     clocks.start()
