@@ -454,22 +454,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
-      const size_t ws_row_stride = (size_t)BN;
-      const int ws_row = (int)cta_rank * BM + q * 32 + (int)lane;  // row within the pair tile
+      // Stream-K partials are kept warp-interleaved: the (cluster, CTA, warp)
+      // slab is NSUB x 8 x 32 float4 with lane fastest, so every store and the
+      // finisher's matching load is one contiguous 512-byte warp access.
+      constexpr int kSlab = C::NSUB * 8 * 32;  // float4 per warp slab
+      const size_t my_slab = (((size_t)cluster_id * CG + cta_rank) * 4 + q) * kSlab;
       if (w.kind == 1) {
         // partial head of a stream-K tile: fp32 to this cluster's workspace
         // slot, then a release flag per epilogue warp
-        float* dst = p.ws + ((size_t)cluster_id * (BM * CG) + ws_row) * ws_row_stride;
+        float4* dst = reinterpret_cast<float4*>(p.ws) + my_slab + lane;
 #pragma unroll 1
         for (int j = 0; j < C::NSUB; ++j) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(t_row + j * C::SUB, v);
           tmem_ld_wait();
-          float4* d4 = reinterpret_cast<float4*>(dst + j * C::SUB);
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            d4[c] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
-                                __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+            __stcg(dst + (j * 8 + c) * 32,
+                   make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                               __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3])));
         }
         tc_fence_before();
         __threadfence();
@@ -500,11 +503,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(t_row + j * C::SUB, v);
         tmem_ld_wait();
         for (int c = c_lo; c <= c_hi; ++c) {
-          const float4* s4 = reinterpret_cast<const float4*>(
-              p.ws + ((size_t)c * (BM * CG) + ws_row) * ws_row_stride + j * C::SUB);
+          const float4* s4 = reinterpret_cast<const float4*>(p.ws) +
+                             (((size_t)c * CG + cta_rank) * 4 + q) * kSlab + j * 8 * 32 + lane;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float4 f = __ldcg(s4 + e);
+            const float4 f = __ldcg(s4 + e * 32);
             v[4 * e] = __float_as_uint(__uint_as_float(v[4 * e]) + f.x);
             v[4 * e + 1] = __float_as_uint(__uint_as_float(v[4 * e + 1]) + f.y);
             v[4 * e + 2] = __float_as_uint(__uint_as_float(v[4 * e + 2]) + f.z);
