@@ -106,6 +106,32 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
                size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
                int dtype, const int* chunk_order, uint64_t epoch, void* stream);
 
+/* One-sided primitives, stream-ordered on the rank's stream: the Table-1
+ * subset the standalone collectives are composed of (reference
+ * primitives.py:126-257).  putmem copies nbytes from the rank's device memory
+ * into `peer`'s replica at dst_off (copy engine over NVLink); getmem the
+ * reverse.  signal_op: op 0 = SET (stream write, release), 1 = ADD (device
+ * red.release.sys).  signal_wait: cond 0 EQ, 1 NE, 2 GE, 3 GT, 4 LE, 5 LT on the
+ * rank's own pad (EQ/GE on the GPU front end, others a one-thread bounded spin). */
+#define SH_SIG_SET 0
+#define SH_SIG_ADD 1
+int sh_putmem(sh_world* w, int rank, int peer, size_t dst_off, const void* src, size_t nbytes,
+              void* stream);
+int sh_getmem(sh_world* w, int rank, void* dst, int peer, size_t src_off, size_t nbytes,
+              void* stream);
+int sh_signal_op(sh_world* w, int rank, int peer, int sig, int op, uint64_t value, void* stream);
+int sh_signal_wait(sh_world* w, int rank, int sig, int cond, uint64_t value, void* stream);
+
+/* out[i] = sum over s = 0..nslots-1 (ascending) of slot s of the rank's own
+ * replica at staging_off (reduce half of rs_intra_streams, collectives.py:163-171).
+ * dtype: SH_DTYPE_BF16 / FP16 (fp32 accumulate), SH_DTYPE_FP32, SH_DTYPE_I32,
+ * SH_DTYPE_I64 (accumulate in the element type, like numpy's `acc +=`). */
+#define SH_DTYPE_FP32 2
+#define SH_DTYPE_I32 3
+#define SH_DTYPE_I64 4
+int sh_reduce_slots(sh_world* w, int rank, size_t staging_off, int nslots, size_t slot_elems,
+                    int dtype, void* out, void* stream);
+
 /* The GEMM core alone (TP=1, no symmetric heap): c(m,n) = a(m,k) @ b(k,n). */
 int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream);
 

@@ -51,6 +51,13 @@ from .pipelines import (
     make_ag_gemm_buffers,
     make_gemm_rs_buffers,
 )
+from .collectives import (
+    ChunkLayout,
+    allgather_pull_intra,
+    allgather_push_intra,
+    reducescatter_push_intra,
+)
+from .primitives import SignalOp, Token, WaitCond, consume_token
 from .swizzle import TileSchedule, TileStep, ag_order_fullmesh, ag_order_switch, rs_inter_order
 
 __all__ = [
@@ -60,7 +67,8 @@ __all__ = [
     "SynchronizationFault", "TileSchedule", "TileStep", "UsageError", "World", "WorldSpec",
     "ag_gemm", "ag_order_fullmesh", "ag_order_switch", "exchange_ipc_handles", "gemm",
     "gemm_rs", "init_world", "init_world_dist", "make_ag_gemm_buffers", "make_gemm_rs_buffers",
-    "rs_inter_order",
+    "rs_inter_order", "ChunkLayout", "allgather_pull_intra", "allgather_push_intra",
+    "reducescatter_push_intra", "SignalOp", "Token", "WaitCond", "consume_token",
 ]
 
 __version__ = "0.1.0"

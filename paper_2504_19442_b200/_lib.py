@@ -34,6 +34,11 @@ SH_ERR_CONFIG = 6
 
 SH_DTYPE_BF16 = 0
 SH_DTYPE_FP16 = 1
+SH_DTYPE_FP32 = 2
+SH_DTYPE_I32 = 3
+SH_DTYPE_I64 = 4
+SH_SIG_SET = 0
+SH_SIG_ADD = 1
 SH_MAX_WORLD = 16
 
 _c_int_p = ctypes.POINTER(ctypes.c_int)
@@ -70,6 +75,16 @@ SIGNATURES = {
     "sh_gemm_rs": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_int, _c_int_p, ctypes.c_uint64, _vp]),
+    "sh_putmem": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, _vp,
+                                 ctypes.c_size_t, _vp]),
+    "sh_getmem": (ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_size_t,
+                                 ctypes.c_size_t, _vp]),
+    "sh_signal_op": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_uint64, _vp]),
+    "sh_signal_wait": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_uint64, _vp]),
+    "sh_reduce_slots": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_size_t, ctypes.c_int,
+                                       ctypes.c_size_t, ctypes.c_int, _vp, _vp]),
     "sh_gemm": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                ctypes.c_int, _vp]),
     "sh_set_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),

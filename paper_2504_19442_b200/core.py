@@ -140,7 +140,124 @@ class Pe:
 
     def barrier_all(self):
         """Host-side rendezvous of every rank (plus device drain)."""
+        self.world.bump(self.rank, "barrier_all")
         self.world._barrier(self)
+
+    # ------------------------------------------------------------------
+    # one-sided primitives (reference primitives.py:126-257), stream-ordered
+
+    def _stream_handle(self):
+        import torch
+
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _payload(self, src, src_off=0, nbytes=None):
+        """Device bytes of ``src`` (bytes / numpy / torch tensor)."""
+        import numpy as np
+        import torch
+
+        if isinstance(src, torch.Tensor):
+            t = src.contiguous().view(-1).view(torch.uint8)
+        else:
+            buf = src.tobytes() if isinstance(src, np.ndarray) else bytes(src)
+            t = torch.frombuffer(bytearray(buf), dtype=torch.uint8) if buf else \
+                torch.empty(0, dtype=torch.uint8)
+        n = t.numel() - src_off if nbytes is None else nbytes
+        if src_off < 0 or n < 0 or src_off + n > t.numel():
+            raise RangeError(f"source range [{src_off}, {src_off + n}) outside {t.numel()} bytes")
+        t = t[src_off:src_off + n]
+        if t.device.type != "cuda":
+            t = t.to(self.torch_device)
+        return t
+
+    def _check_peer(self, peer):
+        if peer < 0 or peer >= self.world.world_size:
+            raise ArgumentError(f"peer {peer} out of range (world {self.world.world_size})")
+
+    def _check_sig(self, sig):
+        if sig < 0 or sig >= self.world.spec.signal_count:
+            raise ArgumentError(f"signal {sig} out of pad of {self.world.spec.signal_count}")
+
+    def putmem(self, dst: SymHandle, src, peer, *, nbytes=None, dst_off=0, src_off=0):
+        """Copy ``src`` into ``peer``'s replica of ``dst`` (copy engine, NVLink)."""
+        self._check_peer(peer)
+        payload = self._payload(src, src_off, nbytes)
+        dst.check(dst_off, payload.numel())
+        self.world.bump(self.rank, "putmem")
+        _lib.check(self.world._lib.sh_putmem(self.world.handle, self.rank, peer,
+                                             dst.offset + dst_off, payload.data_ptr(),
+                                             payload.numel(), self._stream_handle()))
+        return payload  # keep alive until the caller's stream passes the copy
+
+    def getmem(self, dst, src: SymHandle, peer, *, nbytes=None, dst_off=0, src_off=0):
+        """Copy ``peer``'s replica of ``src`` into ``dst`` (a CUDA tensor or the
+        rank's own replica of a SymHandle)."""
+        import torch
+
+        self._check_peer(peer)
+        if isinstance(dst, SymHandle):
+            n = (dst.length - dst_off) if nbytes is None else nbytes
+            dst.check(dst_off, n)
+            src.check(src_off, n)
+            out_ptr = self.world.heap_ptr(self.rank, dst, dst_off)
+        else:
+            if not isinstance(dst, torch.Tensor) or not dst.is_cuda:
+                raise ArgumentError("getmem destination must be a CUDA tensor or SymHandle")
+            flat = dst.view(-1).view(torch.uint8)
+            n = (flat.numel() - dst_off) if nbytes is None else nbytes
+            if dst_off + n > flat.numel():
+                raise RangeError("getmem destination too small")
+            src.check(src_off, n)
+            out_ptr = flat.data_ptr() + dst_off
+        self.world.bump(self.rank, "getmem")
+        _lib.check(self.world._lib.sh_getmem(self.world.handle, self.rank, out_ptr, peer,
+                                             src.offset + src_off, n, self._stream_handle()))
+
+    def signal_op(self, peer, sig, op, value):
+        from .primitives import SignalOp
+
+        self._check_peer(peer)
+        self._check_sig(sig)
+        self.world.bump(self.rank, "signal_op")
+        code = _lib.SH_SIG_SET if op == SignalOp.SET else _lib.SH_SIG_ADD
+        _lib.check(self.world._lib.sh_signal_op(self.world.handle, self.rank, peer, sig, code,
+                                                int(value), self._stream_handle()))
+
+    def notify(self, peer, sig, value):
+        from .primitives import SignalOp
+
+        self.signal_op(peer, sig, SignalOp.SET, value)
+
+    def signal_wait_until(self, sig, cond, value, timeout=None):
+        """The rank's stream waits until its own signal satisfies ``cond``."""
+        self._check_sig(sig)
+        self.world.bump(self.rank, "signal_wait_until")
+        _lib.check(self.world._lib.sh_signal_wait(self.world.handle, self.rank, sig, cond.code,
+                                                  int(value), self._stream_handle()))
+        return value
+
+    def wait(self, sig, value, timeout=None):
+        from .primitives import Token, WaitCond
+
+        self.world.bump(self.rank, "wait")
+        self.signal_wait_until(sig, WaitCond.EQ, value, timeout=timeout)
+        return Token(sig, value)
+
+    def signal_read(self, sig):
+        """Current value of the rank's own signal (synchronises the stream)."""
+        import torch
+
+        torch.cuda.current_stream(self.device).synchronize()
+        return self.world.sig_read(self.rank, sig)
+
+    def local_view(self, handle: SymHandle, dtype=None, shape=None):
+        """Zero-copy CUDA view of this rank's replica of ``handle``."""
+        import torch
+
+        dtype = dtype or torch.uint8
+        if shape is None:
+            shape = (handle.length // torch.empty((), dtype=dtype).element_size(),)
+        return self.world.heap_view(self.rank, handle, dtype, shape)
 
     def __repr__(self):
         return f"Pe(rank={self.rank}, device=cuda:{self.device})"

@@ -729,6 +729,46 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
   }
 }
 
+// Generic slot reduction for the standalone ReduceScatter (any element
+// type): out[i] = sum_{s ascending} slot_s[i], accumulated in Acc.
+template <typename T, typename Acc>
+__global__ void __launch_bounds__(256) slots_reduce_kernel(const T* __restrict__ staging,
+                                                           T* __restrict__ out, size_t slot_elems,
+                                                           int nslots) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < slot_elems;
+       i += (size_t)gridDim.x * blockDim.x) {
+    Acc acc = Acc(0);
+    for (int s = 0; s < nslots; ++s) acc += Acc(staging[(size_t)s * slot_elems + i]);
+    out[i] = T(acc);
+  }
+}
+
+// Bounded spin for the wait conditions the front end cannot evaluate.
+__global__ void flag_wait_cond_kernel(const uint64_t* flag, int cond, uint64_t value, int* err,
+                                      uint64_t timeout_ns) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0 = globaltimer();
+  for (uint32_t i = 1;; ++i) {
+    const uint64_t v = ld_acquire_sys(flag);
+    const bool ok = cond == 0 ? v == value : cond == 1 ? v != value : cond == 2 ? v >= value
+                  : cond == 3 ? v > value : cond == 4 ? v <= value : v < value;
+    if (ok) return;
+    if ((i & 255) == 0 && err && *reinterpret_cast<volatile int*>(err) != 0) return;
+    if (globaltimer() - t0 > timeout_ns) {
+      if (err) atomicCAS(err, 0, 4);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
+__global__ void flag_add_kernel(uint64_t* flag, uint64_t value) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    red_add_release_sys(flag, value);
+  }
+}
+
 // Flag publication: one release store per peer (the signal_op(SET) of
 // reference collectives.py:97 / :161 for a whole chunk).
 __global__ void flag_store_kernel(uint64_t* const* ptrs, int count, uint64_t value) {

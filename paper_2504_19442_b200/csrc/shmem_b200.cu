@@ -338,7 +338,14 @@ int preload_kernels(int dev) {
   // the max-shared-memory carveout: an SM configured for L1 cannot take a
   // GEMM CTA (~225 KB smem) until it drains, and a drained SM is exactly
   // what a spinning reduction would be waiting for.
-  const void* small[] = {reinterpret_cast<const void*>(rs_reduce_kernel<false>),
+  const void* small[] = {reinterpret_cast<const void*>(slots_reduce_kernel<__nv_bfloat16, float>),
+                         reinterpret_cast<const void*>(slots_reduce_kernel<__half, float>),
+                         reinterpret_cast<const void*>(slots_reduce_kernel<float, float>),
+                         reinterpret_cast<const void*>(slots_reduce_kernel<int32_t, int32_t>),
+                         reinterpret_cast<const void*>(slots_reduce_kernel<long long, long long>),
+                         reinterpret_cast<const void*>(flag_wait_cond_kernel),
+                         reinterpret_cast<const void*>(flag_add_kernel),
+                         reinterpret_cast<const void*>(rs_reduce_kernel<false>),
                          reinterpret_cast<const void*>(rs_reduce_kernel<true>),
                          reinterpret_cast<const void*>(flag_store_kernel),
                          reinterpret_cast<const void*>(flag_store_list_kernel),
@@ -1084,6 +1091,121 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   CUDA_TRY(cudaGetLastError());
 
   return store_flags(s, fl, nfl, epoch);
+}
+
+// ---------------------------------------------------------------------------
+// one-sided primitives + slot reduction (standalone collectives)
+
+int sh_putmem(sh_world* w, int rank, int peer, size_t dst_off, const void* src, size_t nbytes,
+              void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (peer < 0 || peer >= w->world || !rs->peer[peer])
+    return fail(SH_ERR_ARG, "peer %d out of range (world %d)", peer, w->world);
+  if (dst_off + nbytes > w->heap_bytes)
+    return fail(SH_ERR_ARG, "put [%zu, %zu) outside heap of %zu", dst_off, dst_off + nbytes,
+                w->heap_bytes);
+  if (nbytes == 0) return SH_OK;
+  if (!src) return fail(SH_ERR_ARG, "null source");
+  CUDA_TRY(cudaSetDevice(rs->device));
+  CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(rs->peer[peer]) + dst_off, src, nbytes,
+                           cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return SH_OK;
+}
+
+int sh_getmem(sh_world* w, int rank, void* dst, int peer, size_t src_off, size_t nbytes,
+              void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (peer < 0 || peer >= w->world || !rs->peer[peer])
+    return fail(SH_ERR_ARG, "peer %d out of range (world %d)", peer, w->world);
+  if (src_off + nbytes > w->heap_bytes)
+    return fail(SH_ERR_ARG, "get [%zu, %zu) outside heap of %zu", src_off, src_off + nbytes,
+                w->heap_bytes);
+  if (nbytes == 0) return SH_OK;
+  if (!dst) return fail(SH_ERR_ARG, "null destination");
+  CUDA_TRY(cudaSetDevice(rs->device));
+  CUDA_TRY(cudaMemcpyAsync(dst, static_cast<char*>(rs->peer[peer]) + src_off, nbytes,
+                           cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return SH_OK;
+}
+
+int sh_signal_op(sh_world* w, int rank, int peer, int sig, int op, uint64_t value, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (peer < 0 || peer >= w->world || !rs->peer[peer])
+    return fail(SH_ERR_ARG, "peer %d out of range (world %d)", peer, w->world);
+  if (sig < 0 || sig >= w->signal_count)
+    return fail(SH_ERR_ARG, "signal %d out of pad of %d", sig, w->signal_count);
+  CUDA_TRY(cudaSetDevice(rs->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint64_t* f = sig_addr(w, *rs, peer, sig);
+  if (op == SH_SIG_SET) return store_flags(s, &f, 1, value);
+  if (op != SH_SIG_ADD) return fail(SH_ERR_ARG, "unknown signal op %d", op);
+  flag_add_kernel<<<1, 32, 0, s>>>(f, value);
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_signal_wait(sh_world* w, int rank, int sig, int cond, uint64_t value, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (sig < 0 || sig >= w->signal_count)
+    return fail(SH_ERR_ARG, "signal %d out of pad of %d", sig, w->signal_count);
+  if (cond < 0 || cond > 5) return fail(SH_ERR_ARG, "unknown wait condition %d", cond);
+  CUDA_TRY(cudaSetDevice(rs->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t* f = sig_addr(w, *rs, rank, sig);
+  Driver& d = driver();
+  if (d.wait64 && (cond == 0 || cond == 2)) {
+    CUresult r = d.wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(f), value,
+                          cond == 0 ? CU_STREAM_WAIT_VALUE_EQ : CU_STREAM_WAIT_VALUE_GEQ);
+    if (r == CUDA_SUCCESS) return SH_OK;
+  }
+  flag_wait_cond_kernel<<<1, 32, 0, s>>>(f, cond, value, rs->err_dev, w->timeout_ns);
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_reduce_slots(sh_world* w, int rank, size_t staging_off, int nslots, size_t slot_elems,
+                    int dtype, void* out, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  static const size_t esize[] = {2, 2, 4, 4, 8};
+  if (dtype < 0 || dtype > 4) return fail(SH_ERR_ARG, "dtype %d not supported", dtype);
+  if (nslots < 1) return fail(SH_ERR_ARG, "need at least one slot");
+  if (staging_off + (size_t)nslots * slot_elems * esize[dtype] > w->heap_bytes)
+    return fail(SH_ERR_ARG, "staging outside heap");
+  if (slot_elems == 0) return SH_OK;
+  if (!out) return fail(SH_ERR_ARG, "null output");
+  CUDA_TRY(cudaSetDevice(rs->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const void* st = static_cast<char*>(rs->peer[rank]) + staging_off;
+  int grid = (int)std::min<size_t>((slot_elems + 255) / 256, (size_t)num_sms(rs->device) * 4);
+  switch (dtype) {
+    case SH_DTYPE_BF16:
+      slots_reduce_kernel<__nv_bfloat16, float><<<grid, 256, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(st), static_cast<__nv_bfloat16*>(out), slot_elems,
+          nslots);
+      break;
+    case SH_DTYPE_FP16:
+      slots_reduce_kernel<__half, float><<<grid, 256, 0, s>>>(
+          static_cast<const __half*>(st), static_cast<__half*>(out), slot_elems, nslots);
+      break;
+    case SH_DTYPE_FP32:
+      slots_reduce_kernel<float, float><<<grid, 256, 0, s>>>(
+          static_cast<const float*>(st), static_cast<float*>(out), slot_elems, nslots);
+      break;
+    case SH_DTYPE_I32:
+      slots_reduce_kernel<int32_t, int32_t><<<grid, 256, 0, s>>>(
+          static_cast<const int32_t*>(st), static_cast<int32_t*>(out), slot_elems, nslots);
+      break;
+    default:
+      slots_reduce_kernel<long long, long long><<<grid, 256, 0, s>>>(
+          static_cast<const long long*>(st), static_cast<long long*>(out), slot_elems, nslots);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
 }
 
 }  // extern "C"
