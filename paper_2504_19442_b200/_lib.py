@@ -88,6 +88,7 @@ SIGNATURES = {
     "sh_gemm": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                ctypes.c_int, _vp]),
     "sh_set_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "sh_set_schedule_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "sh_query_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int_p,
                                             _c_int_p, _c_int_p]),
 }

@@ -104,6 +104,8 @@ int env_int(const char* name, int dflt) {
 
 std::atomic<int> g_force_bn{0};
 std::atomic<int> g_force_cg{0};
+std::atomic<int> g_stream_k{-2};  // -2: not set (env SHB_SK or auto), -1 auto, 0 off, 1 on
+std::atomic<int> g_group_m{-1};   // -1: not set (env SHB_GROUP_M or auto), 0 auto, >0 fixed
 
 int num_sms(int dev) {
   static int cache[64] = {0};
@@ -125,11 +127,15 @@ struct Cfg {
 // clusters (the rest stays one-tile-per-cluster).  Returns dp_tiles.
 int stream_k_split(const Cfg& c, int num_kb) {
   const int clusters = c.grid / c.cg;
-  const char* env = getenv("SHB_SK");
-  if (env && atoi(env) == 0) return c.tiles;
+  int mode = g_stream_k.load();  // -1 auto, 0 off, 1 on
+  if (mode == -2) {
+    const char* env = getenv("SHB_SK");
+    mode = env ? (atoi(env) != 0 ? 1 : 0) : -1;
+  }
+  if (mode == 0) return c.tiles;
   const int waves = (c.tiles + clusters - 1) / clusters;
   const double eff = double(c.tiles) / double(waves * clusters);
-  const bool want = env ? atoi(env) != 0 : (eff < 0.92 && num_kb >= 8);
+  const bool want = mode == 1 || (eff < 0.92 && num_kb >= 8);
   if (!want || c.tiles <= 0) return c.tiles;
   const int full = c.tiles / clusters;
   return full > 1 ? (full - 1) * clusters : 0;
@@ -172,7 +178,10 @@ int sk_reserve(SkWorkspace& w, int clusters, int cg, int bn) {
 // per 8 m-blocks.  Less DRAM traffic = less power = higher clocks under the
 // 1 kW cap (measured: the GEMM runs power-limited).
 int raster_group(int rows, int k, int mblk, int bm) {
-  if (const char* e = getenv("SHB_GROUP_M")) return std::max(1, std::min(mblk, atoi(e)));
+  const int forced = g_group_m.load();
+  if (forced > 0) return std::max(1, std::min(mblk, forced));
+  if (const char* e = getenv("SHB_GROUP_M"); e && forced < 0)
+    return std::max(1, std::min(mblk, atoi(e)));
   // B200's L2 behaves like ~2 x 63 MB (one partition per die) for data that
   // every SM touches, so budget well under 63 MB for the resident A rows
   const double budget = 32.0 * (1 << 20);
@@ -746,6 +755,14 @@ int sh_set_tile_config(int bn, int cta_group) {
   if (cta_group < 0 || cta_group > 2) return fail(SH_ERR_ARG, "cta_group must be 0, 1 or 2");
   g_force_bn = bn;
   g_force_cg = cta_group;
+  return SH_OK;
+}
+
+int sh_set_schedule_config(int stream_k, int group_m) {
+  if (stream_k < -1 || stream_k > 1) return fail(SH_ERR_ARG, "stream_k must be -1, 0 or 1");
+  if (group_m < 0) return fail(SH_ERR_ARG, "group_m must be >= 0");
+  g_stream_k = stream_k;
+  g_group_m = group_m;
   return SH_OK;
 }
 
