@@ -132,6 +132,16 @@ int sh_signal_wait(sh_world* w, int rank, int sig, int cond, uint64_t value, voi
 int sh_reduce_slots(sh_world* w, int rank, size_t staging_off, int nslots, size_t slot_elems,
                     int dtype, void* out, void* stream);
 
+/* Timeline evidence (reference World.start_trace/stop_trace, core.py:434-444,
+ * and Timeline.to_chrome_trace, costmodel.py:185-190): while enabled, every
+ * fused launch of `rank` records %globaltimer stamps per CTA -- chunk-flag
+ * waits, per-tile epilogue windows, peer-arrival waits, CTA lifetime -- into
+ * a ring of `max_launches` launch slots.  sh_trace_read copies the ring
+ * (words = max_launches*grid*records_per_cta*4) and fills info =
+ * {launches recorded, slots, grid, records_per_cta, mode of slot 0..}. */
+int sh_trace_enable(sh_world* w, int rank, int records_per_cta, int max_launches);
+int sh_trace_read(sh_world* w, int rank, uint64_t* out_host, size_t out_words, int* info);
+
 /* The GEMM core alone (TP=1, no symmetric heap): c(m,n) = a(m,k) @ b(k,n). */
 int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream);
 

@@ -85,6 +85,8 @@ SIGNATURES = {
                                       ctypes.c_uint64, _vp]),
     "sh_reduce_slots": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_size_t, ctypes.c_int,
                                        ctypes.c_size_t, ctypes.c_int, _vp, _vp]),
+    "sh_trace_enable": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "sh_trace_read": (ctypes.c_int, [_vp, ctypes.c_int, _c_u64_p, ctypes.c_size_t, _c_int_p]),
     "sh_gemm": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                ctypes.c_int, _vp]),
     "sh_set_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),

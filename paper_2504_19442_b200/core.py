@@ -510,6 +510,19 @@ class World:
                 c.clear()
 
     # ------------------------------------------------------------------
+    # timeline (reference core.py:434-444; device stamps, see timeline.py)
+
+    def start_trace(self, records_per_cta=512, launches=16):
+        from .timeline import start_trace
+
+        start_trace(self, records_per_cta, launches)
+
+    def stop_trace(self):
+        from .timeline import stop_trace
+
+        return stop_trace(self)
+
+    # ------------------------------------------------------------------
     # device error words
 
     def poll_error(self, rank):

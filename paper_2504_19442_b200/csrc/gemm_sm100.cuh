@@ -51,6 +51,13 @@ struct TileParams {
   int copy_own;                       // AG: store own-chunk A stages into gathered[rank]
   uint16_t* own_slot_ptr;             // AG: gathered[rank] (rows x k)
   int dbg;                            // experiment switches (0 in production)
+  // optional timeline: per CTA `trace_cap` records of 4 u64 {kind|aux, t0, t1, tile}
+  // (%globaltimer ns); producer records fill from the front, epilogue (warp 2)
+  // records from the middle.  Kinds: 1 chunk-flag wait (AG), 2 tile
+  // epilogue (t0 = accumulator ready, t1 = stores issued), 3 peer-arrival
+  // wait (fused RS), 4 CTA lifetime.
+  uint64_t* trace;
+  int trace_cap;
   // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
   // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
   // clusters.  A cluster's range is walked backwards, so the partial head of a
@@ -63,6 +70,16 @@ struct TileParams {
   int* err;                           // host-mapped error word
   uint64_t timeout_ns;
 };
+
+__device__ __forceinline__ void trace_rec(const TileParams& p, int slot, uint64_t kind_aux,
+                                          uint64_t t0, uint64_t t1, uint64_t tile) {
+  if (slot >= p.trace_cap) return;
+  uint64_t* r = p.trace + ((size_t)blockIdx.x * p.trace_cap + slot) * 4;
+  r[0] = kind_aux;
+  r[1] = t0;
+  r[2] = t1;
+  r[3] = tile;
+}
 
 struct WorkItem {
   int t, kb0, kb1, kind;  // kind: 0 whole tile, 1 partial head (to workspace), 2 finishing tail
@@ -241,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       uint32_t stage = 0, phase = 0;
       uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
+      int trace_slot = 1;   // slot 0: CTA lifetime (written by the epilogue)
       uint32_t copy_mask = 0, stored_phase = 0;  // stages holding an own-slot copy
       const uint64_t b_hint = (p.dbg & 8) ? kEvictLast : kEvictNormal;
       WorkIter wi;
@@ -256,8 +274,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (MODE == MODE_AG && !own && !((landed >> chunk) & 1u)) {
           // wait(ready[chunk]) of pipelines.py:130-141, as an acquire spin
           if (lane == 0) {
+            const uint64_t tw0 = p.trace ? globaltimer() : 0;
             spin_geq(p.ready + chunk, p.epoch, p.err, p.timeout_ns, 1);
             fence_proxy_async_global();
+            if (p.trace) trace_rec(p, trace_slot++, (1ull << 56) | chunk, tw0, globaltimer(), w.t);
           }
           __syncwarp();
           landed |= 1u << chunk;
@@ -416,6 +436,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int pend_chunk = -1;    // RS: tile whose stores still have to be published
     uint64_t pend_count = 0;
     const size_t slot_elems = (size_t)p.rows * p.n;
+    const bool tracer = p.trace != nullptr && warp == 2 && lane == 0;
+    const uint64_t t_cta0 = tracer ? globaltimer() : 0;
+    int trace_slot = p.trace_cap / 2;
     WorkIter wi;
     wi.init(p, cluster_id, num_clusters, num_kb);
     WorkItem w;
@@ -446,13 +469,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the reduce side of rs_intra_streams (collectives.py:163-171) for my
         // own chunk: every other source's rows must have landed; every lane
         // acquires so its own loads below are ordered after the releases
+        const uint64_t tw0 = tracer ? globaltimer() : 0;
         for (int s = 0; s < p.world; ++s)
           if (s != p.rank) spin_geq(p.rs_mine + s, p.rs_target, p.err, p.timeout_ns, 3);
         __syncwarp();
+        if (tracer) trace_rec(p, trace_slot++, (3ull << 56) | chunk, tw0, globaltimer(), w.t);
         peers_in = true;
       }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
+      const uint64_t t_acc = tracer ? globaltimer() : 0;
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       // Stream-K partials are kept warp-interleaved: the (cluster, CTA, warp)
       // slab is NSUB x 8 x 32 float4 with lane fastest, so every store and the
@@ -483,6 +509,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_release_sys(p.ws_flags + ((size_t)cluster_id * CG + cta_rank) * 4 + q, p.ws_epoch);
         }
         __syncwarp();
+        if (tracer)
+          trace_rec(p, trace_slot++, (2ull << 56) | (1ull << 32) | (uint64_t)chunk, t_acc,
+                    globaltimer(), w.t);
         continue;
       }
       int c_lo = 0, c_hi = -1;  // clusters holding this tile's earlier k-blocks
@@ -623,6 +652,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           buf = (pair ^ 1) * 2;
         }
       }
+      if (tracer)
+        trace_rec(p, trace_slot++, (2ull << 56) | ((uint64_t)w.kind << 32) | (uint64_t)chunk, t_acc,
+                  globaltimer(), w.t);
       if constexpr (MODE == MODE_RS) {
         // Publish the previous tile of a peer chunk now that this tile's
         // stores are queued behind it (keeps the store-completion wait off
@@ -647,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
+    if (tracer) trace_rec(p, 0, (4ull << 56) | blockIdx.x, t_cta0, globaltimer(), 0);
     if (lane == 0) {
       bulk_wait<0>();
       if (MODE == MODE_RS && pend_chunk >= 0) {

@@ -383,6 +383,16 @@ int ensure_preloaded(int dev) {
   return SH_OK;
 }
 
+template <typename RS>
+void attach_trace(RS& rs, TileParams& p, int mode) {
+  if (!rs.trace) return;
+  const int slot = (int)(rs.trace_count % rs.trace_launches);
+  p.trace = rs.trace + (size_t)slot * rs.trace_grid * rs.trace_cap * 4;
+  p.trace_cap = rs.trace_cap;
+  rs.trace_modes[slot] = mode;
+  ++rs.trace_count;
+}
+
 int check_shape(int m, int n, int k, int world, int dtype) {
   if (m < 1 || n < 1 || k < 1) return fail(SH_ERR_ARG, "m, n, k must be >= 1");
   if (world < 1 || world > SH_MAX_WORLD)
@@ -416,6 +426,10 @@ struct RankState {
   bool shares_gpu = false;  // another rank of this process uses the same device
   int ranks_on_device = 1;  // ranks of this process on `device` (incl. this one)
   SkWorkspace sk;           // stream-K partials of this rank's AG launches
+  uint64_t* trace = nullptr;  // [max_launches][grid_max][cap][4] timeline records
+  int trace_cap = 0, trace_launches = 0, trace_grid = 0;
+  long long trace_count = 0;  // launches recorded so far
+  std::vector<int> trace_modes;
 };
 
 struct sh_world {
@@ -657,6 +671,7 @@ int sh_world_destroy(sh_world* w) {
     if (rs.ev_in) cudaEventDestroy(rs.ev_in);
     if (rs.ev_done) cudaEventDestroy(rs.ev_done);
     if (rs.err_host) cudaFreeHost(rs.err_host);
+    if (rs.trace) cudaFree(rs.trace);
     if (rs.sk.ws) cudaFree(rs.sk.ws);
     if (rs.sk.flags) cudaFree(rs.sk.flags);
   }
@@ -755,6 +770,44 @@ int sh_set_tile_config(int bn, int cta_group) {
   if (cta_group < 0 || cta_group > 2) return fail(SH_ERR_ARG, "cta_group must be 0, 1 or 2");
   g_force_bn = bn;
   g_force_cg = cta_group;
+  return SH_OK;
+}
+
+int sh_trace_enable(sh_world* w, int rank, int records_per_cta, int max_launches) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  CUDA_TRY(cudaSetDevice(rs->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (rs->trace) cudaFree(rs->trace);
+  rs->trace = nullptr;
+  rs->trace_count = 0;
+  if (records_per_cta <= 0 || max_launches <= 0) return SH_OK;
+  rs->trace_cap = records_per_cta;
+  rs->trace_launches = max_launches;
+  rs->trace_grid = num_sms(rs->device);
+  rs->trace_modes.assign(max_launches, -1);
+  const size_t bytes = (size_t)max_launches * rs->trace_grid * records_per_cta * 4 * 8;
+  CUDA_TRY(cudaMalloc(&rs->trace, bytes));
+  CUDA_TRY(cudaMemset(rs->trace, 0, bytes));
+  return SH_OK;
+}
+
+int sh_trace_read(sh_world* w, int rank, uint64_t* out_host, size_t out_words, int* info) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (!rs->trace) return fail(SH_ERR_STATE, "tracing is not enabled on rank %d", rank);
+  const size_t words = (size_t)rs->trace_launches * rs->trace_grid * rs->trace_cap * 4;
+  if (out_words < words) return fail(SH_ERR_ARG, "need %zu words", words);
+  CUDA_TRY(cudaSetDevice(rs->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(out_host, rs->trace, words * 8, cudaMemcpyDeviceToHost));
+  if (info) {  // {launches recorded, slots, grid, cap, mode of slot 0..}
+    info[0] = (int)rs->trace_count;
+    info[1] = rs->trace_launches;
+    info[2] = rs->trace_grid;
+    info[3] = rs->trace_cap;
+    for (int i = 0; i < rs->trace_launches; ++i) info[4 + i] = rs->trace_modes[i];
+  }
   return SH_OK;
 }
 
@@ -951,6 +1004,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
+  attach_trace(*rs, p, MODE_AG);
   p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
   if (p.dp_tiles < p.num_tiles) {
     if ((rc = sk_reserve(rs->sk, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
@@ -1075,6 +1129,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   const size_t slot_elems = (size_t)rows * n;
   const uint64_t target = epoch * (uint64_t)slot_elems;
   p.dp_tiles = p.num_tiles;  // RS tiles publish per chunk; no stream-K split
+  attach_trace(*rs, p, MODE_RS);
   p.rs_mine = sig_addr(w, *rs, rank, reduction_base);
   p.rs_target = target;
   p.staging_local = staging;
