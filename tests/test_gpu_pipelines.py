@@ -349,3 +349,52 @@ def test_ag_gemm_stream_k_tail_exact(rng, monkeypatch, world_size):
                 assert np.array_equal(out, ref)
             gathered = to_np(w.read_tensor(r, bufs.gathered, BF16, (shape.m, shape.k)))
             assert np.array_equal(gathered, oracle.gathered_layout(shards))
+
+
+@pytest.mark.parametrize("world_size,rows,n,k", [(3, 200, 200, 72), (2, 130, 264, 520),
+                                                 (5, 64, 136, 40), (1, 1000, 1000, 1000)])
+def test_ragged_shapes_ag_and_rs_exact(rng, world_size, rows, n, k):
+    # rows / n / k that are not multiples of the 256 x 256 x 64 tiles, odd worlds:
+    # TMA clips the edges, chunk boundaries never mix (3D maps)
+    m = rows * world_size
+    ag_shape = ProblemShape(m=m, n=n, k=k, dtype="bfloat16")
+    rs_shape = ProblemShape(m=m, n=n, k=k, dtype="bfloat16")
+    with make_world(world_size, heap_bytes=1 << 26) as w:
+        agb, rsb = make_ag_gemm_buffers(w, ag_shape), make_gemm_rs_buffers(w, rs_shape)
+        shards = [ints(rng, -2, 3, (rows, k)) for _ in range(world_size)]
+        amats = [ints(rng, -1, 2, (m, k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (k, n))
+        ag_ref = oracle.ag_gemm_reference(shards, b)
+        rs_ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+        assert np.abs(ag_ref).max() < 256 and max(np.abs(r).max() for r in rs_ref) < 256
+
+        def body(pe):
+            x, a, bb = dev(shards[pe.rank], pe), dev(amats[pe.rank], pe), dev(b, pe)
+            h = ag_gemm(pe, x, bb, ag_shape, ag_order_switch(pe.rank, world_size), agb)
+            y = gemm_rs(pe, a, bb, rs_shape, rs_inter_order(pe.ctx, 1, world_size), rsb)
+            return h, y
+
+        for r, (h, y) in enumerate(run_np(w, body)):
+            assert np.array_equal(h, ag_ref)
+            assert np.array_equal(y, rs_ref[r])
+            staging = to_np(w.read_tensor(r, rsb.staging, BF16, (world_size, rows, n)))
+            assert np.array_equal(staging, oracle.staging_layout(amats, [b] * world_size, r))
+            gathered = to_np(w.read_tensor(r, agb.gathered, BF16, (m, k)))
+            assert np.array_equal(gathered, oracle.gathered_layout(shards))
+
+
+def test_unaligned_row_length_rejected():
+    # rows must be 16-byte TMA strides: n % 8 / k % 8 != 0 is an ArgumentError,
+    # never a silent CPU fallback
+    shape = ProblemShape(m=256, n=12, k=64, dtype="bfloat16")
+    with make_world(1) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+
+        def body(pe):
+            a = torch.zeros((256, 64), dtype=BF16, device=pe.torch_device)
+            b = torch.zeros((64, 12), dtype=BF16, device=pe.torch_device)
+            return ag_gemm(pe, a, b, shape, ag_order_switch(0, 1), bufs)
+
+        with pytest.raises(CollectiveFault) as info:
+            w.run(body)
+        assert isinstance(info.value.first, ArgumentError)
