@@ -49,8 +49,6 @@ struct TileParams {
   const uint16_t* staging_local;      // RS: my staging buffer (W slots of rows x n)
   int fuse_reduce;                    // RS: reduce my chunk in the epilogue of its tiles
   int copy_own;                       // AG: store own-chunk A stages into gathered[rank]
-  uint16_t* own_slot_ptr;             // AG: gathered[rank] (rows x k)
-  int dbg;                            // experiment switches (0 in production)
   // optional timeline: per CTA `trace_cap` records of 4 u64 {kind|aux, t0, t1, tile}
   // (%globaltimer ns); producer records fill from the front, epilogue (warp 2)
   // records from the middle.  Kinds: 1 chunk-flag wait (AG), 2 tile
@@ -260,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
       int trace_slot = 1;   // slot 0: CTA lifetime (written by the epilogue)
       uint32_t copy_mask = 0, stored_phase = 0;  // stages holding an own-slot copy
-      const uint64_t b_hint = (p.dbg & 8) ? kEvictLast : kEvictNormal;
+      const uint64_t b_hint = kEvictNormal;
       WorkIter wi;
       wi.init(p, cluster_id, num_clusters, num_kb);
       WorkItem w;
@@ -285,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (((copy_mask >> stage) & 1u) && !(p.dbg & 2)) {
+          if ((copy_mask >> stage) & 1u) {
             // the own-slot store of the previous occupant must have read it
             mbar_wait(&stored_bar[stage], (stored_phase >> stage) & 1u);
             stored_phase ^= 1u << stage;
@@ -296,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // CTA-local barrier; the copier forwards the bytes to the leader's
           // full barrier and keeps the stage until its store has read it.
           bool copy_kb = false;
-          if (copying && !(p.dbg & 32)) {
+          if (copying) {
             copy_kb = cr == 0;
             cr = (cr + 1 == p.nblk) ? 0 : cr + 1;
             if (copy_kb) copy_mask |= 1u << stage;
@@ -396,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (wi.next(w)) {
         int chunk, mb, nb;
         decode_tile(p, w.t, chunk, mb, nb);
-        const bool copying = chunk == p.rank && !(p.dbg & 32);
+        const bool copying = chunk == p.rank;
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
         int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
@@ -409,12 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_complete_tx_cluster(&full[stage], 0, C::A_BYTES);  // hand to the MMA
               // evict-first: 1 B written per 2 B the GEMM keeps reading from
               // L2; don't let the copy push the operands out
-              if (!(p.dbg & 16)) {
-                tma_store_2d_hint(&maps.own_slot, sA + stage * C::A_BYTES, kb * BK, row0,
-                                  (p.dbg & 4) ? kEvictNormal : kEvictFirst);
-                bulk_commit();
-                bulk_wait_read<0>();
-              }
+              tma_store_2d_hint(&maps.own_slot, sA + stage * C::A_BYTES, kb * BK, row0,
+                                kEvictFirst);
+              bulk_commit();
+              bulk_wait_read<0>();
               mbar_arrive(&stored_bar[stage]);
             }
             cr = (cr + 1 == p.nblk) ? 0 : cr + 1;

@@ -508,18 +508,23 @@ int store_flags(cudaStream_t s, uint64_t* const* ptrs, int count, uint64_t value
   // Stream memory operation (executed by the GPU front end, no SM needed,
   // implicit memory barrier before the write = data-before-flag); the
   // one-warp release-store kernel is the fallback.
+  // Writes are idempotent SETs, so flags a stream write could not take (e.g.
+  // a peer mapping the front end rejects) simply go to the kernel as well.
+  static std::atomic<bool> write_value_broken{false};
   Driver& d = driver();
-  if (d.write64 && !env_int("SHB_FLAG_KERNEL", 0)) {
-    bool ok = true;
-    for (int i = 0; i < count && ok; ++i)
-      ok = d.write64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(ptrs[i]), value,
-                     CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS;
-    if (ok) return SH_OK;
-    if (count > 1) return fail(SH_ERR_CUDA, "cuStreamWriteValue64 failed midway");
-  }
   FlagList l;
-  for (int i = 0; i < count; ++i) l.ptr[i] = ptrs[i];
-  flag_store_list_kernel<<<1, 32, 0, s>>>(l, count, value);
+  int nk = 0;
+  const bool try_wv = d.write64 && !write_value_broken.load() && !env_int("SHB_FLAG_KERNEL", 0);
+  for (int i = 0; i < count; ++i) {
+    if (try_wv && d.write64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(ptrs[i]),
+                            value, CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS)
+      continue;
+    if (try_wv) write_value_broken = true;
+    l.ptr[nk++] = ptrs[i];
+  }
+  if (nk == 0) return SH_OK;
+  cudaGetLastError();  // a rejected stream write may leave a sticky-free error behind
+  flag_store_list_kernel<<<1, 32, 0, s>>>(l, nk, value);
   CUDA_TRY(cudaGetLastError());
   return SH_OK;
 }
@@ -1013,8 +1018,6 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     p.ws_epoch = ++rs->sk.epoch;
   }
   p.copy_own = own_by_ce ? 0 : 1;
-  p.dbg = env_int("SHB_DBG", 0);
-  p.own_slot_ptr = reinterpret_cast<uint16_t*>(own_gathered + (size_t)rank * chunk_bytes);
   if (p.copy_own) {
     uint64_t d[2] = {(uint64_t)k, (uint64_t)rows}, st[1] = {(uint64_t)k * es};
     uint32_t bx[2] = {64, 128};
