@@ -398,3 +398,44 @@ def test_unaligned_row_length_rejected():
         with pytest.raises(CollectiveFault) as info:
             w.run(body)
         assert isinstance(info.value.first, ArgumentError)
+
+
+def test_criterion_6_pipeline_correctness_on_gpu():
+    # reference tests/test_acceptance.py:418-486 on the GPU path: W in {1,2,4,8},
+    # ProblemShape(64, 32, 32, tile_m=4, tile_n=16), four schedules, seed 77;
+    # payloads in [-1, 1] keep every product and sum exact in bf16
+    from paper_2504_19442_b200 import ag_order_fullmesh
+
+    rng = np.random.default_rng(77)
+    for world_size in (1, 2, 4, 8):
+        shape = ProblemShape(m=64, n=32, k=32, dtype="bfloat16", tile_m=4, tile_n=16)
+        rows = shape.rows_per_rank(world_size)
+        with make_world(world_size, heap_bytes=1 << 20) as w:
+            ag_bufs, rs_bufs = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+            shards = [ints(rng, -1, 2, (rows, shape.k)) for _ in range(world_size)]
+            amats = [ints(rng, -1, 2, (shape.m, shape.k)) for _ in range(world_size)]
+            b = ints(rng, -1, 2, (shape.k, shape.n))
+            ag_ref = np.vstack(shards) @ b
+            rs_ref = sum(a @ b for a in amats)
+            perm = list(rng.permutation(world_size))
+            schedules = [
+                lambda pe: ag_order_switch(pe.rank, world_size),
+                lambda pe: rs_inter_order(pe.ctx, 1, world_size),
+                lambda pe: perm_schedule(pe.rank, perm),
+                lambda pe: ag_order_fullmesh(pe.rank, world_size, 1),
+            ]
+            outs = []
+            for make_sched in schedules:
+                def body(pe):
+                    x, a, bb = dev(shards[pe.rank], pe), dev(amats[pe.rank], pe), dev(b, pe)
+                    return (ag_gemm(pe, x, bb, shape, make_sched(pe), ag_bufs),
+                            gemm_rs(pe, a, bb, shape, make_sched(pe), rs_bufs))
+
+                res = run_np(w, body)
+                for r, (h, y) in enumerate(res):
+                    assert np.array_equal(h, ag_ref)
+                    assert np.array_equal(y, rs_ref[r * rows:(r + 1) * rows])
+                outs.append(res)
+            for other in outs[1:]:  # bit-identical across schedules
+                for (h0, y0), (h1, y1) in zip(outs[0], other):
+                    assert np.array_equal(h0, h1) and np.array_equal(y0, y1)
