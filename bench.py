@@ -424,6 +424,7 @@ def main():
                      "frac_of_burst": achieved / burst, "frac_of_sustained": achieved / sustained,
                      "per_launch_algorithmic_bytes": (AG["m"] * AG["k"] * 2 * 2 + AG["k"] * AG["n"] * 2
                                                       + AG["m"] * AG["n"] * 2)},
+        "tp_roofline": tp_roofline(N, peak, ag_ms, rs_ms, ms),
         "e2e": {"value": STEP_FLOPS * N / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                 "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": rows * RS["n"] * 2,
                 "ms_per_step": e2e_ms,
@@ -441,6 +442,31 @@ def main():
     world.close()
     if N > 1:
         dist.destroy_process_group()
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def tp_roofline(n_gpus, peak_tflops, ag_ms, rs_ms, step_ms):
+    """BASELINE.json's roofline: per op the slower of the GEMM at the tensor
+    peak and the shard bytes that must cross NVLink (AG in: (TP-1)/TP*M*K*2,
+    RS out: (TP-1)/TP*M*N*2), and the measured fraction of it."""
+    tp = n_gpus
+    t_gemm_ag = flops(AG) / (peak_tflops * 1e12) * 1e6
+    t_gemm_rs = flops(RS) / (peak_tflops * 1e12) * 1e6
+    t_nvl_ag = (tp - 1) / tp * AG["m"] * AG["k"] * 2 / (NVLINK_GBS * 1e9) * 1e6
+    t_nvl_rs = (tp - 1) / tp * RS["m"] * RS["n"] * 2 / (NVLINK_GBS * 1e9) * 1e6
+    r_ag, r_rs = max(t_gemm_ag, t_nvl_ag), max(t_gemm_rs, t_nvl_rs)
+    return {
+        "ag": {"t_gemm_us": t_gemm_ag, "t_nvlink_us": t_nvl_ag,
+               "bound": "tensor" if t_gemm_ag >= t_nvl_ag else "nvlink",
+               "measured_us": ag_ms * 1e3, "frac": r_ag / (ag_ms * 1e3)},
+        "rs": {"t_gemm_us": t_gemm_rs, "t_nvlink_us": t_nvl_rs,
+               "bound": "tensor" if t_gemm_rs >= t_nvl_rs else "nvlink",
+               "measured_us": rs_ms * 1e3, "frac": r_rs / (rs_ms * 1e3)},
+        "step_frac": (r_ag + r_rs) / (step_ms * 1e3),
+        "peak_tflops": peak_tflops, "nvlink_gbs": NVLINK_GBS,
+    }
 
 
 def ctypes_query_tile(_lib, rows, world, n):

@@ -446,6 +446,22 @@ class World:
         torch.cuda.synchronize(self.devices[viewer])
         return out
 
+    def copy_into(self, rank, handle: SymHandle, off, payload, chunked=None):
+        """Write ``payload`` into ``rank``'s replica of ``handle``, synchronously
+        (reference core.py:306-324; ``chunked`` is the CPU scheduler's knob and
+        has no meaning here)."""
+        import torch
+
+        viewer = self._local_rank_for(rank)
+        pe = self.pes[viewer]
+        with torch.cuda.device(pe.device):
+            data = pe._payload(payload)
+            handle.check(off, data.numel())
+            stream = torch.cuda.current_stream(pe.device)
+            _lib.check(self._lib.sh_putmem(self._handle, viewer, rank, handle.offset + off,
+                                           data.data_ptr(), data.numel(), stream.cuda_stream))
+            stream.synchronize()
+
     def read_from(self, rank, handle: SymHandle, off, nbytes):
         """Bytes of rank's replica (reference core.py:326-328)."""
         import torch

@@ -210,3 +210,11 @@ def test_primitives_put_get_signal_roundtrip():
         res = w.run(body)
         assert res[0].cpu().tolist() == [2] * 32 and res[1].cpu().tolist() == [1] * 32
         assert w.sig_read(0, sigs.at(1)) == 5 and w.sig_read(1, sigs.at(0)) == 5
+
+
+def test_world_copy_into_and_read_from():
+    with make_world(2) as w:
+        h = w.alloc_symmetric(16)
+        w.copy_into(1, h, 4, b"abcdefgh")
+        assert w.read_from(1, h, 4, 8) == b"abcdefgh"
+        assert w.read_from(0, h, 0, 16) == bytes(16)
