@@ -142,8 +142,14 @@ int sh_reduce_slots(sh_world* w, int rank, size_t staging_off, int nslots, size_
 int sh_trace_enable(sh_world* w, int rank, int records_per_cta, int max_launches);
 int sh_trace_read(sh_world* w, int rank, uint64_t* out_host, size_t out_words, int* info);
 
-/* The GEMM core alone (TP=1, no symmetric heap): c(m,n) = a(m,k) @ b(k,n). */
-int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream);
+/* The GEMM core alone (TP=1, no symmetric heap): c(m,n) = a(m,k) @ b(k,n).
+ * `workspace` (device, 16-B aligned, sh_gemm_workspace_bytes() bytes, may be
+ * NULL when that is 0) holds the stream-K partials; with a NULL / short
+ * workspace the kernel falls back to whole tiles.  Stream-ordered like the
+ * rest, so a caching allocator may hand the same block to the next call. */
+int sh_gemm_workspace_bytes(int m, int n, int k, size_t* bytes);
+int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* workspace,
+            size_t workspace_bytes, void* stream);
 
 /* Tile override for tuning: bn in {0 (auto), 128, 224, 256}; cta_group in {0 (auto), 1, 2}
  * (224 needs cta_group 2). */
@@ -152,6 +158,9 @@ int sh_set_tile_config(int bn, int cta_group);
  * they would leave CTA pairs idle), 0 off, 1 always; group_m 0 auto (L2
  * budget) or the number of m-blocks walked per n-block. */
 int sh_set_schedule_config(int stream_k, int group_m);
+/* Data-parallel tile hand-out: -1 default (env SHB_DYN, else static), 0 static
+ * stride schedule, 1 dynamic (global atomic counter, one tile fetched ahead). */
+int sh_set_dynamic_tiles(int mode);
 /* Launch config chosen for a problem (for the bench's roofline bookkeeping). */
 int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid);
 

@@ -87,10 +87,13 @@ SIGNATURES = {
                                        ctypes.c_size_t, ctypes.c_int, _vp, _vp]),
     "sh_trace_enable": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "sh_trace_read": (ctypes.c_int, [_vp, ctypes.c_int, _c_u64_p, ctypes.c_size_t, _c_int_p]),
+    "sh_gemm_workspace_bytes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                               _c_size_p]),
     "sh_gemm": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                               ctypes.c_int, _vp]),
+                               ctypes.c_int, _vp, ctypes.c_size_t, _vp]),
     "sh_set_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "sh_set_schedule_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "sh_set_dynamic_tiles": (ctypes.c_int, [ctypes.c_int]),
     "sh_query_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int_p,
                                             _c_int_p, _c_int_p]),
 }

@@ -56,12 +56,19 @@ struct TileParams {
   // wait (fused RS), 4 CTA lifetime.
   uint64_t* trace;
   int trace_cap;
+  uint64_t l2_hint_a, l2_hint_b;      // TMA L2 cache policies of the operand loads
   // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
   // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
   // clusters.  A cluster's range is walked backwards, so the partial head of a
   // tile is produced first and the cluster finishing its tail (k_end = K)
   // reduces the partials from the fp32 workspace.
   int dp_tiles;
+  // dynamic scheduling of the data-parallel tiles: the leader CTA's producer
+  // claims tile ids from a global counter (zeroed before the launch) and
+  // broadcasts them through a small smem ring to every role of the pair, so
+  // the tiles in flight stay a compact window in launch order (L2 reuse) and
+  // faster clusters take more tiles.  The stream-K tail stays static.
+  int* tile_counter;                  // null: static stride schedule
   float* ws;                          // clusters x (CG*128) x BN fp32 partials
   uint64_t* ws_flags;                 // clusters x CG x 4 epilogue warps
   uint64_t ws_epoch;                  // launch counter of this workspace
@@ -83,11 +90,29 @@ struct WorkItem {
   int t, kb0, kb1, kind;  // kind: 0 whole tile, 1 partial head (to workspace), 2 finishing tail
 };
 
+constexpr int kRing = 4;
+
+// Tile-id ring of the dynamic scheduler (one per CTA, same smem offset in
+// both CTAs of a pair; `empty` is only used in the leader CTA).
+struct TileRing {
+  int ids[kRing];
+  uint64_t full[kRing];
+  uint64_t empty[kRing];
+};
+
 // Identical sequence of work items for the producer, MMA and epilogue roles.
+// role: 0 = fetcher (leader producer), 1 = consumer warp, 2 = not a ring user
 struct WorkIter {
   int t, C, KB, dp;
   long long u0, u, U;
-  __device__ __forceinline__ void init(const TileParams& p, int cid, int nclusters, int kb) {
+  // dynamic phase
+  TileRing* ring;
+  int* counter;
+  int role, rslot, cg, pending;
+  uint32_t rphase;
+  bool dyn;
+  __device__ __forceinline__ void init(const TileParams& p, int cid, int nclusters, int kb,
+                                       TileRing* r = nullptr, int ring_role = 2, int cgs = 1) {
     C = nclusters;
     KB = kb;
     dp = p.dp_tiles;
@@ -95,9 +120,58 @@ struct WorkIter {
     U = (long long)(p.num_tiles - dp) * KB;
     u0 = U * cid / C;
     u = U * (cid + 1) / C;
+    ring = r;
+    counter = p.tile_counter;
+    role = ring_role;
+    cg = cgs;
+    rslot = 0;
+    rphase = 0;
+    dyn = counter != nullptr && dp > 0;
+    // the first tile of every cluster is static (cid); later ones come from
+    // the counter, fetched one tile ahead so the atomic's latency is hidden
+    pending = cid;
+  }
+  // next data-parallel tile id from the ring (-1: exhausted); warp-wide call
+  __device__ __forceinline__ int ring_next() {
+    const uint32_t lane = threadIdx.x & 31;
+    int id = -1;
+    if (role == 0) {
+      mbar_wait_cluster(&ring->empty[rslot], rphase ^ 1);
+      if (lane == 0) {
+        id = pending < dp ? pending : -1;
+        if (id >= 0) pending = C + atomicAdd(counter, 1);
+        ring->ids[rslot] = id;
+        if (cg == 2) {
+          asm volatile(
+              "{\n\t.reg .b32 ra;\n\t"
+              "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
+              "st.shared::cluster.u32 [ra], %1;\n\t}" ::"r"(smem_u32(&ring->ids[rslot])),
+              "r"(id)
+              : "memory");
+          mbar_arrive_cluster(&ring->full[rslot], 1);
+        }
+        mbar_arrive(&ring->full[rslot]);
+      }
+      id = __shfl_sync(0xffffffffu, id, 0);
+    } else {
+      mbar_wait_cluster(&ring->full[rslot], rphase);
+      id = *reinterpret_cast<volatile int*>(&ring->ids[rslot]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&ring->empty[rslot], 0);
+    }
+    if (++rslot == kRing) { rslot = 0; rphase ^= 1; }
+    return id;
   }
   __device__ __forceinline__ bool next(WorkItem& w) {
-    if (t < dp) {
+    if (dyn) {
+      const int id = ring_next();
+      if (id >= 0) {
+        w.t = id; w.kb0 = 0; w.kb1 = KB; w.kind = 0;
+        return true;
+      }
+      dyn = false;
+      t = dp;  // data-parallel tiles exhausted: continue with the stream-K range
+    } else if (t < dp) {
       w.t = t; w.kb0 = 0; w.kb1 = KB; w.kind = 0;
       t += C;
       return true;
@@ -208,7 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* stored_bar = tempty + 2;        // AG own copy: copier done with stage s
   uint64_t* alanded_bar = stored_bar + STAGES;  // AG own copy: this CTA's A half landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(alanded_bar + STAGES);
+  TileRing* ring = reinterpret_cast<TileRing*>(alanded_bar + STAGES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 1);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -237,6 +312,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&stored_bar[s], 1);
       mbar_init(&alanded_bar[s], 1);
     }
+    // ring consumers per CTA: 4 epilogue warps + (MMA warp in the leader /
+    // producer warp in the peer) + the own-slot copier when it runs
+    const int per_cta = 5 + ((MODE == MODE_AG && p.copy_own) ? 1 : 0);
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&ring->full[r], 1);
+      mbar_init(&ring->empty[r], per_cta * CG);
+    }
     fence_mbarrier_init();
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
@@ -258,9 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
       int trace_slot = 1;   // slot 0: CTA lifetime (written by the epilogue)
       uint32_t copy_mask = 0, stored_phase = 0;  // stages holding an own-slot copy
-      const uint64_t b_hint = kEvictNormal;
+      const uint64_t b_hint = p.l2_hint_b, a_hint = p.l2_hint_a;
       WorkIter wi;
-      wi.init(p, cluster_id, num_clusters, num_kb);
+      wi.init(p, cluster_id, num_clusters, num_kb, ring, leader ? 0 : 1, CG);
       WorkItem w;
       while (wi.next(w)) {
         int chunk, mb, nb;
@@ -306,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (leader) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES * CG);
             if (copy_kb) {
               mbar_arrive_expect_tx(&alanded_bar[stage], C::A_BYTES);
-              tma_load_2d(&maps.a_own, &alanded_bar[stage], a_dst, kx, row0, kEvictNormal);
+              tma_load_2d(&maps.a_own, &alanded_bar[stage], a_dst, kx, row0, a_hint);
 #pragma unroll
               for (int j = 0; j < C::B_BOXES; ++j) {
                 if constexpr (CG == 1)
@@ -317,15 +399,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    kx, b_hint);
               }
             } else if constexpr (CG == 1) {
-              if (own) tma_load_2d(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
-              else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+              if (own) tma_load_2d(&maps.a_own, &full[stage], a_dst, kx, row0, a_hint);
+              else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, a_hint);
 #pragma unroll
               for (int j = 0; j < C::B_BOXES; ++j)
                 tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
                             b_hint);
             } else {
-              if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, kEvictNormal);
-              else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, kEvictNormal);
+              if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, a_hint);
+              else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, a_hint);
 #pragma unroll
               for (int j = 0; j < C::B_BOXES; ++j)
                 tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
@@ -352,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t stage = 0, phase = 0;
       int it = 0;
       WorkIter wi;
-      wi.init(p, cluster_id, num_clusters, num_kb);
+      wi.init(p, cluster_id, num_clusters, num_kb, ring, 1, CG);
       WorkItem w;
       for (; wi.next(w); ++it) {
         const int as = it & 1;
@@ -386,10 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // smem for the MMA, so 1/nblk of them (k-block kb of n-block kb mod nblk
     // -- each k-block of each m-block exactly once) are copied from smem into
     // gathered[rank] once the MMAs consumed them.  No extra HBM or L2 reads.
-    if (MODE == MODE_AG && p.copy_own && lane == 0) {
+    if (MODE == MODE_AG && p.copy_own) {  // whole warp walks the items, lane 0 copies
       uint32_t stage = 0, landed_phase = 0;
       WorkIter wi;
-      wi.init(p, cluster_id, num_clusters, num_kb);
+      wi.init(p, cluster_id, num_clusters, num_kb, ring, 1, CG);
       WorkItem w;
       while (wi.next(w)) {
         int chunk, mb, nb;
@@ -399,11 +481,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           if (copying) {
-            if (cr == 0) {
+            if (cr == 0 && lane == 0) {
               // uses of a stage for copies alternate with `stored` acks, so
               // this parity wait is never more than one phase away
               mbar_wait(&alanded_bar[stage], (landed_phase >> stage) & 1u);
-              landed_phase ^= 1u << stage;
               mbar_complete_tx_cluster(&full[stage], 0, C::A_BYTES);  // hand to the MMA
               // evict-first: 1 B written per 2 B the GEMM keeps reading from
               // L2; don't let the copy push the operands out
@@ -413,12 +494,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               bulk_wait_read<0>();
               mbar_arrive(&stored_bar[stage]);
             }
+            if (cr == 0) landed_phase ^= 1u << stage;
             cr = (cr + 1 == p.nblk) ? 0 : cr + 1;
           }
           if (++stage == STAGES) stage = 0;
         }
+        __syncwarp();
       }
-      bulk_wait<0>();
+      if (lane == 0) bulk_wait<0>();
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
@@ -436,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t t_cta0 = tracer ? globaltimer() : 0;
     int trace_slot = p.trace_cap / 2;
     WorkIter wi;
-    wi.init(p, cluster_id, num_clusters, num_kb);
+    wi.init(p, cluster_id, num_clusters, num_kb, ring, 1, CG);
     WorkItem w;
     for (; wi.next(w); ++it) {
       int chunk, mb, nb;

@@ -299,9 +299,20 @@ int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaS
   return launch_one<128, 1, MODE, FP16>(maps, p, c.grid, s);
 }
 
+uint64_t l2_policy(const char* env, uint64_t dflt) {
+  const char* v = getenv(env);
+  if (!v) return dflt;
+  if (!strcmp(v, "first")) return kEvictFirst;
+  if (!strcmp(v, "last")) return kEvictLast;
+  return kEvictNormal;
+}
+
 template <int MODE>
-int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParams& p,
+int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParams& pin,
                 cudaStream_t s) {
+  TileParams p = pin;
+  p.l2_hint_a = l2_policy("SHB_HINT_A", kEvictNormal);
+  p.l2_hint_b = l2_policy("SHB_HINT_B", kEvictNormal);
   if (env_int("SHB_TRACE", 0))
     fprintf(stderr,
             "[shb] mode=%d bn=%d cg=%d grid=%d rows=%d n=%d k=%d W=%d rank=%d mblk=%d nblk=%d "
@@ -383,6 +394,32 @@ int ensure_preloaded(int dev) {
   return SH_OK;
 }
 
+std::atomic<int> g_dynamic{-1};  // -1: not set (env SHB_DYN, default off), 0 off, 1 on
+
+// Dynamic (atomic-counter) hand-out of the data-parallel tiles.  Off by
+// default: for uniform tiles the static stride schedule gives every cluster
+// exactly the same tile count, which the static stream-K split after it
+// assumes; measured on C3 the dynamic variant reads ~2% less DRAM but loses
+// ~3% tensor-pipe utilisation to the uneven per-cluster tile counts.
+bool dynamic_tiles() {
+  const int forced = g_dynamic.load();
+  if (forced >= 0) return forced != 0;
+  const char* e = getenv("SHB_DYN");
+  return e ? atoi(e) != 0 : false;
+}
+
+// Zero the tile counter on the stream.  A stream memory write runs on the GPU
+// front end (no SM): a memset kernel could be starved by spinning GEMMs of
+// sibling ranks sharing the GPU, which wait on this very launch.
+int zero_counter(int* counter, cudaStream_t s) {
+  Driver& d = driver();
+  if (d.write64 && d.write64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(counter),
+                             0, CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS)
+    return SH_OK;
+  CUDA_TRY(cudaMemsetAsync(counter, 0, 8, s));
+  return SH_OK;
+}
+
 template <typename RS>
 void attach_trace(RS& rs, TileParams& p, int mode) {
   if (!rs.trace) return;
@@ -426,6 +463,7 @@ struct RankState {
   bool shares_gpu = false;  // another rank of this process uses the same device
   int ranks_on_device = 1;  // ranks of this process on `device` (incl. this one)
   SkWorkspace sk;           // stream-K partials of this rank's AG launches
+  int* tile_counter = nullptr;  // dynamic tile scheduler counter (zeroed per launch)
   uint64_t* trace = nullptr;  // [max_launches][grid_max][cap][4] timeline records
   int trace_cap = 0, trace_launches = 0, trace_grid = 0;
   long long trace_count = 0;  // launches recorded so far
@@ -453,6 +491,8 @@ int init_rank_common(sh_world* w, RankState& rs) {
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(rs.device));
   if ((rc = sk_reserve(rs.sk, num_sms(rs.device) / 2, 2, 256))) return rc;
+  CUDA_TRY(cudaMalloc(&rs.tile_counter, 256));
+  CUDA_TRY(cudaMemset(rs.tile_counter, 0, 256));
   CUDA_TRY(cudaStreamCreateWithFlags(&rs.comm, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_in, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_done, cudaEventDisableTiming));
@@ -677,6 +717,7 @@ int sh_world_destroy(sh_world* w) {
     if (rs.ev_done) cudaEventDestroy(rs.ev_done);
     if (rs.err_host) cudaFreeHost(rs.err_host);
     if (rs.trace) cudaFree(rs.trace);
+    if (rs.tile_counter) cudaFree(rs.tile_counter);
     if (rs.sk.ws) cudaFree(rs.sk.ws);
     if (rs.sk.flags) cudaFree(rs.sk.flags);
   }
@@ -824,6 +865,12 @@ int sh_set_schedule_config(int stream_k, int group_m) {
   return SH_OK;
 }
 
+int sh_set_dynamic_tiles(int mode) {
+  if (mode < -1 || mode > 1) return fail(SH_ERR_ARG, "mode must be -1, 0 or 1");
+  g_dynamic = mode;
+  return SH_OK;
+}
+
 int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -837,7 +884,28 @@ int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, in
 // ---------------------------------------------------------------------------
 // plain GEMM core (TP = 1)
 
-int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* stream) {
+// Caller-provided stream-K workspace: fp32 partial slabs + one flag word per
+// (cluster, CTA, epilogue warp), zeroed per launch on the caller's stream.
+size_t sk_workspace_bytes(const Cfg& c) {
+  const size_t clusters = c.grid / c.cg;
+  return clusters * c.cg * 128 * (size_t)c.bn * sizeof(float) + clusters * c.cg * 4 * 8;
+}
+
+constexpr size_t kCounterBytes = 256;  // dynamic tile counter at the front of the workspace
+
+int sh_gemm_workspace_bytes(int m, int n, int k, size_t* bytes) {
+  if (!bytes) return fail(SH_ERR_ARG, "null argument");
+  if (m < 1 || n < 1 || k < 1) return fail(SH_ERR_ARG, "m, n, k must be >= 1");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Cfg cfg = choose_cfg(m, 1, n, num_sms(dev));
+  *bytes = kCounterBytes +
+           (stream_k_split(cfg, (k + 63) / 64) < cfg.tiles ? sk_workspace_bytes(cfg) : 0);
+  return SH_OK;
+}
+
+int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* workspace,
+            size_t workspace_bytes, void* stream) {
   int rc = check_shape(m, n, k, 1, dtype);
   if (rc) return rc;
   if (!a || !b || !c) return fail(SH_ERR_ARG, "null tensor");
@@ -879,15 +947,24 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
   p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const bool have_ws = workspace && aligned16(workspace) && workspace_bytes >= kCounterBytes;
+  if (have_ws && dynamic_tiles()) {
+    p.tile_counter = static_cast<int*>(workspace);
+    if ((rc = zero_counter(p.tile_counter, cs))) return rc;
+  }
   if (p.dp_tiles < p.num_tiles) {
-    static std::mutex mu;
-    static std::map<std::pair<int, void*>, SkWorkspace> pool;
-    std::lock_guard<std::mutex> g(mu);
-    SkWorkspace& ws = pool[{dev, stream}];
-    if ((rc = sk_reserve(ws, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
-    p.ws = ws.ws;
-    p.ws_flags = ws.flags;
-    p.ws_epoch = ++ws.epoch;
+    const size_t need = sk_workspace_bytes(cfg);
+    if (!have_ws || workspace_bytes < kCounterBytes + need) {
+      p.dp_tiles = p.num_tiles;  // no (or too small a) workspace: plain tiles
+    } else {
+      char* base = static_cast<char*>(workspace) + kCounterBytes;
+      const size_t slabs = need - (size_t)(cfg.grid / cfg.cg) * cfg.cg * 4 * 8;
+      p.ws = reinterpret_cast<float*>(base);
+      p.ws_flags = reinterpret_cast<uint64_t*>(base + slabs);
+      p.ws_epoch = 1;
+      CUDA_TRY(cudaMemsetAsync(p.ws_flags, 0, need - slabs, cs));
+    }
   }
   p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
   p.order[0] = 0;
@@ -1010,6 +1087,10 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
   attach_trace(*rs, p, MODE_AG);
+  if (dynamic_tiles()) {
+    p.tile_counter = rs->tile_counter;
+    if ((rc = zero_counter(rs->tile_counter, s))) return rc;
+  }
   p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
   if (p.dp_tiles < p.num_tiles) {
     if ((rc = sk_reserve(rs->sk, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
@@ -1133,6 +1214,10 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   const uint64_t target = epoch * (uint64_t)slot_elems;
   p.dp_tiles = p.num_tiles;  // RS tiles publish per chunk; no stream-K split
   attach_trace(*rs, p, MODE_RS);
+  if (dynamic_tiles()) {
+    p.tile_counter = rs->tile_counter;
+    if ((rc = zero_counter(rs->tile_counter, s))) return rc;
+  }
   p.rs_mine = sig_addr(w, *rs, rank, reduction_base);
   p.rs_target = target;
   p.staging_local = staging;

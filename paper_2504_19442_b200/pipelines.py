@@ -13,8 +13,8 @@ call through the C ABI (include/shmem_b200.h):
 * ``gemm_rs(pe, a (m, k), b (k, n), shape, schedule, bufs)`` returns row block
   ``rank`` of ``sum_r a_r @ b_r`` (pipelines.py:179-233).  The GEMM epilogue
   stores each bf16 tile straight into the owner's ``staging`` slot ``rank``
-  and release-adds the owner's per-source counter; a vectorised reduction
-  sums the W slots in ascending source order.
+  and release-adds the owner's per-source counter; the epilogue of the own
+  chunk's tiles (scheduled last) sums the W slots in ascending source order.
 
 Data are torch tensors (bf16 or fp16) on the rank's GPU; CPU tensors are
 copied to the GPU first.  Calls are stream-ordered on the current CUDA
@@ -257,8 +257,17 @@ def gemm(a, b):
     b = b.contiguous()
     m, k = a.shape
     n = b.shape[1]
+    import ctypes
+
     c = torch.empty((m, n), dtype=a.dtype, device=a.device)
     code = _lib.SH_DTYPE_FP16 if a.dtype == torch.float16 else _lib.SH_DTYPE_BF16
-    _lib.check(_lib.load().sh_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, code,
-                                   torch.cuda.current_stream(a.device).cuda_stream))
+    lib = _lib.load()
+    with torch.cuda.device(a.device):
+        need = ctypes.c_size_t()
+        _lib.check(lib.sh_gemm_workspace_bytes(m, n, k, ctypes.byref(need)))
+        # stream-K partials: a stream-ordered block from torch's caching allocator
+        ws = torch.empty(need.value, dtype=torch.uint8, device=a.device) if need.value else None
+        _lib.check(lib.sh_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m, n, k, code,
+                               ws.data_ptr() if ws is not None else None, need.value,
+                               torch.cuda.current_stream(a.device).cuda_stream))
     return c

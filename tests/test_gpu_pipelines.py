@@ -326,10 +326,13 @@ def test_tp_mlp_float_tolerance():
         assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-2
 
 
+@pytest.mark.parametrize("dyn", ["0", "1"])
 @pytest.mark.parametrize("world_size", [1, 2])
-def test_ag_gemm_stream_k_tail_exact(rng, monkeypatch, world_size):
-    # enough tiles for the stream-K tail (80 on 74 CTA pairs at W=1)
+def test_ag_gemm_stream_k_tail_exact(rng, monkeypatch, world_size, dyn):
+    # enough tiles for the stream-K tail (80 on 74 CTA pairs at W=1); dyn=1
+    # hands the data-parallel tiles out through the atomic counter
     monkeypatch.setenv("SHB_SK", "1")
+    monkeypatch.setenv("SHB_DYN", dyn)
     shape = ProblemShape(m=2560, n=2048, k=512, dtype="bfloat16")
     rows = shape.m // world_size
     with make_world(world_size, heap_bytes=1 << 26) as w:
@@ -349,6 +352,31 @@ def test_ag_gemm_stream_k_tail_exact(rng, monkeypatch, world_size):
                 assert np.array_equal(out, ref)
             gathered = to_np(w.read_tensor(r, bufs.gathered, BF16, (shape.m, shape.k)))
             assert np.array_equal(gathered, oracle.gathered_layout(shards))
+
+
+@pytest.mark.parametrize("dyn", ["0", "1"])
+@pytest.mark.parametrize("world_size", [1, 2])
+def test_gemm_rs_stream_k_tail_exact(rng, monkeypatch, world_size, dyn):
+    # the fused RS epilogue behind stream-K partial tiles: finishers publish
+    # the summed tile into the peers' staging slots
+    monkeypatch.setenv("SHB_SK", "1")
+    monkeypatch.setenv("SHB_DYN", dyn)
+    shape = ProblemShape(m=2560, n=2048, k=512, dtype="bfloat16")
+    with make_world(world_size, heap_bytes=1 << 26) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        amats = [ints(rng, -2, 3, (shape.m, shape.k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (shape.k, shape.n))
+        ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+        assert max(np.abs(r).max() for r in ref) < 256
+
+        def body(pe):
+            a, bb = dev(amats[pe.rank], pe), dev(b, pe)
+            return [gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, world_size), bufs,
+                            reset=False) for _ in range(2)]
+
+        for r, outs in enumerate(run_np(w, body)):
+            for out in outs:
+                assert np.array_equal(out, ref[r])
 
 
 @pytest.mark.parametrize("world_size,rows,n,k", [(3, 200, 200, 72), (2, 130, 264, 520),

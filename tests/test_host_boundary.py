@@ -40,10 +40,10 @@ def test_argument_errors_without_gpu():
     with pytest.raises(ArgumentError, match="bn must be"):
         _lib.check(rc)
     assert lib.sh_set_tile_config(0, 0) == _lib.SH_OK
-    assert lib.sh_gemm(None, None, None, 0, 8, 8, 0, None) == _lib.SH_ERR_ARG
-    assert lib.sh_gemm(None, None, None, 8, 6, 8, 0, None) == _lib.SH_ERR_ARG  # n % 8
-    assert lib.sh_gemm(None, None, None, 8, 8, 8, 7, None) == _lib.SH_ERR_ARG  # dtype
-    lib.sh_gemm(None, None, None, 8, 6, 8, 0, None)
+    assert lib.sh_gemm(None, None, None, 0, 8, 8, 0, None, 0, None) == _lib.SH_ERR_ARG
+    assert lib.sh_gemm(None, None, None, 8, 6, 8, 0, None, 0, None) == _lib.SH_ERR_ARG  # n % 8
+    assert lib.sh_gemm(None, None, None, 8, 8, 8, 7, None, 0, None) == _lib.SH_ERR_ARG  # dtype
+    lib.sh_gemm(None, None, None, 8, 6, 8, 0, None, 0, None)
     assert b"multiples of 8" in lib.sh_last_error()
     out = ctypes.c_void_p()
     assert lib.sh_world_create(0, None, 1 << 20, 0, 5.0, ctypes.byref(out)) == _lib.SH_ERR_CONFIG
