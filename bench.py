@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps (capped at 50)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-unfused", action="store_true")
+    p.add_argument("--no-sweep", action="store_true", help="skip the C5 TP/M sweep")
     return p.parse_args()
 
 
@@ -242,6 +243,8 @@ def main():
     torch.cuda.set_device(local)
     N = world_env
     heap = (AG["m"] * AG["k"] + RS["m"] * RS["n"]) * 2 + (64 << 20)
+    if not args.no_sweep:
+        heap += sweep_heap_bytes(world_env)
     if N > 1:
         # BENCH_BACKEND=gloo lets several ranks share one GPU (functional check
         # of the N>1 path; NCCL refuses duplicate GPUs)
@@ -395,6 +398,11 @@ def main():
 
     # ------------------------------------------------------------- roofline
     burst, sustained, peak_src = peaks()
+    sweep = None
+    if not args.no_sweep:
+        # short calls (a few ms each): the burst peak is the roofline denominator
+        sweep = run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, burst)
+        world.check_errors(rank)
     dom_ms = ag_ms
     achieved = flops(AG) / (dom_ms * 1e-3) / 1e12
     # the roofline call is timed right after K back-to-back steps: under the
@@ -430,6 +438,7 @@ def main():
                 "ms_per_step": e2e_ms,
                 "how": "pinned X H2D + ag_gemm + gemm_rs + Y D2H per step, double-buffered"},
         "unfused_baseline": unfused,
+        "sweep": sweep,
         "cpu_baseline": cpu,
         "gpu_launches": args.steps * 2,
         "gpu_launches_note": ("per step: gemm_tp_kernel<MODE_AG> + gemm_tp_kernel<MODE_RS> "
@@ -445,6 +454,93 @@ def main():
 
 
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+# C5 of BASELINE.json: TP sweep over M for both ops (Llama-3-70B MLP, N=28672,
+# K=8192 hidden): AG ProblemShape(M, 28672/TP, 8192), RS ProblemShape(M, 8192, 28672/TP)
+SWEEP_M = (1024, 4096, 16384)
+FFN, HID = 28672, 8192
+
+
+def sweep_shapes(tp):
+    for M in SWEEP_M:
+        yield "ag_gemm", M, dict(m=M, n=FFN // tp, k=HID)
+        yield "gemm_rs", M, dict(m=M, n=HID, k=FFN // tp)
+
+
+def sweep_heap_bytes(tp):
+    return sum(s["m"] * (s["k"] if op == "ag_gemm" else s["n"]) * 2 + (1 << 20)
+               for op, _, s in sweep_shapes(tp))
+
+
+def run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, peak):
+    """Both fused ops against the unfused cuBLAS (+ NCCL at N>1) sequence at
+    TP=N for every M of C5; per point TFLOPS/GPU and the fraction of the
+    BASELINE roofline max(GEMM at the tensor peak, shard bytes over NVLink)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = pe.rank
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    w_up = (torch.randn(HID, FFN // N, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    w_dn = (torch.randn(FFN // N, HID, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    ag_sched = sb.ag_order_switch(rank, N)
+    rs_sched = sb.rs_inter_order(world.ranks[rank], 1, N)
+    out = []
+    for op, M, s in sweep_shapes(N):
+        shape = sb.ProblemShape(dtype="bfloat16", **s)
+        fl = flops(s)
+        iters = int(max(5, min(30, 0.08 / (fl / 1.2e15))))
+        if op == "ag_gemm":
+            bufs = sb.make_ag_gemm_buffers(world, shape)
+            x = torch.randn(M // N, HID, device=dev, generator=g).to(torch.bfloat16)
+            ours = lambda: sb.ag_gemm(pe, x, w_up, shape, ag_sched, bufs, reset=False)  # noqa: E731
+            if N > 1:
+                xg = torch.empty((M, HID), dtype=torch.bfloat16, device=dev)
+
+                def unfused():
+                    dist.all_gather_into_tensor(xg, x)
+                    torch.matmul(xg, w_up)
+            else:
+                unfused = lambda: torch.matmul(x, w_up)  # noqa: E731
+            nvl_bytes = (N - 1) / N * M * HID * 2
+        else:
+            bufs = sb.make_gemm_rs_buffers(world, shape)
+            a = torch.randn(M, FFN // N, device=dev, generator=g).to(torch.bfloat16)
+            ours = lambda: sb.gemm_rs(pe, a, w_dn, shape, rs_sched, bufs, reset=False)  # noqa: E731
+            if N > 1:
+                ys = torch.empty((M // N, HID), dtype=torch.bfloat16, device=dev)
+
+                def unfused():
+                    dist.reduce_scatter_tensor(ys, torch.matmul(a, w_dn))
+            else:
+                unfused = lambda: torch.matmul(a, w_dn)  # noqa: E731
+            nvl_bytes = (N - 1) / N * M * HID * 2
+
+        def timed(fn):
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    fn()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(iters):
+                    fn()
+                e1.record(stream)
+                barrier()
+            return max_over_ranks(e0.elapsed_time(e1) / iters)
+
+        ms_ours, ms_unf = timed(ours), timed(unfused)
+        t_gemm = fl / (peak * 1e12) * 1e3
+        t_nvl = nvl_bytes / (NVLINK_GBS * 1e9) * 1e3
+        roof = max(t_gemm, t_nvl)
+        out.append({"op": op, "tp": N, "M": M, "shape": s, "iters": iters,
+                    "ours_us": ms_ours * 1e3, "unfused_us": ms_unf * 1e3,
+                    "ours_tflops_per_gpu": fl / (ms_ours * 1e-3) / 1e12,
+                    "unfused_tflops_per_gpu": fl / (ms_unf * 1e-3) / 1e12,
+                    "bound": "tensor" if t_gemm >= t_nvl else "nvlink",
+                    "roofline_frac": roof / ms_ours, "unfused_roofline_frac": roof / ms_unf})
+        del bufs
+    return out
 
 
 def tp_roofline(n_gpus, peak_tflops, ag_ms, rs_ms, step_ms):

@@ -746,13 +746,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             red_add_release_sys(p.rs_count[pend_chunk], pend_count);
           }
           pend_chunk = -1;
+          // count the elements this warp actually delivered (TMA clips the
+          // ragged edges), so a chunk is complete at exactly rows*n per call
+          const int vr = max(0, min(32, p.rows - row));
+          const int vc = max(0, min(BN, p.n - n0));
           if (!fused_own) {
-            // count the elements this warp actually delivered (TMA clips the
-            // ragged edges), so a chunk is complete at exactly rows*n per call
-            const int vr = max(0, min(32, p.rows - row));
-            const int vc = max(0, min(BN, p.n - n0));
             pend_chunk = chunk;
             pend_count = (uint64_t)vr * (uint64_t)vc;
+          } else {
+            // nobody waits on my own chunk's counter in the fused path, but it
+            // advances all the same, so the counters mean the same thing in
+            // both modes (a later unfused call targets epoch * rows * n)
+            red_add_release_sys(p.rs_count[chunk], (uint64_t)vr * (uint64_t)vc);
           }
         }
         __syncwarp();

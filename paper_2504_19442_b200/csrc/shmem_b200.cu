@@ -171,23 +171,29 @@ int sk_reserve(SkWorkspace& w, int clusters, int cg, int bn) {
   return SH_OK;
 }
 
-// Raster group (m-blocks walked before moving to the next n-block).  If the
-// chunk's A rows fit in ~64 MB of L2 they all stay resident and B streams
-// through exactly once (group = every m-block); otherwise group as many
-// m-blocks as fit, so B is re-read ceil(mblk/group) times instead of once
-// per 8 m-blocks.  Less DRAM traffic = less power = higher clocks under the
-// 1 kW cap (measured: the GEMM runs power-limited).
-int raster_group(int rows, int k, int mblk, int bm) {
+// Raster group (m-blocks walked before moving to the next n-block).  Two
+// regimes:
+//  * short K: a group of m-blocks whose A rows fit in ~32 MB of L2 stays
+//    resident while B streams through once per group (B200's L2 behaves like
+//    ~2 x 63 MB for data that every SM touches, so budget well under 63 MB);
+//  * long K (the A rows of even a few m-blocks exceed the budget): nothing
+//    stays resident across tiles; the reuse comes from the clusters of one
+//    wave walking K in near lockstep, so each k-slice of a block is fetched
+//    once per wave.  DRAM reads per wave ~ (distinct m-blocks + distinct
+//    n-blocks), minimised by a square wave: group ~ sqrt(clusters).
+// Less DRAM traffic = less power = higher clocks under the 1 kW cap.
+int raster_group(int rows, int k, int mblk, int bm, int clusters) {
   const int forced = g_group_m.load();
   if (forced > 0) return std::max(1, std::min(mblk, forced));
   if (const char* e = getenv("SHB_GROUP_M"); e && forced < 0)
     return std::max(1, std::min(mblk, atoi(e)));
-  // B200's L2 behaves like ~2 x 63 MB (one partition per die) for data that
-  // every SM touches, so budget well under 63 MB for the resident A rows
   const double budget = 32.0 * (1 << 20);
   const double a_blk = (double)bm * k * 2;
   if (a_blk * mblk <= budget) return std::max(1, mblk);
-  return std::max(1, std::min(mblk, (int)(budget / a_blk)));
+  const int resident = (int)(budget / a_blk);
+  int square = 1;
+  while ((square + 1) * (square + 1) <= clusters) ++square;
+  return std::max(1, std::min(mblk, std::max(resident, square)));
 }
 
 Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
@@ -201,7 +207,10 @@ Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
   for (int ci = 0; ci < 2; ++ci) {
     int cg = cgs[ci];
     if (g_force_cg && g_force_cg != cg) continue;
-    if (!g_force_cg && cg == 1) continue;  // pairs by default
+    // single-CTA tiles stage 1.5x the operand bytes per flop of a pair tile;
+    // they win only where a 256-row pair tile would be mostly padding (a
+    // chunk of <= 128 rows: TP=8 at M=1024)
+    if (!g_force_cg && cg == 1 && rows > 128) continue;
     for (int bi = 0; bi < 3; ++bi) {
       int bn = bns[bi];
       if (g_force_bn && g_force_bn != bn) continue;
@@ -221,7 +230,8 @@ Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
       // measured on B200: a 256x128 pair tile runs at ~0.6x the per-flop rate
       // of 256x256 (operand smem traffic per MMA doubles), so narrow tiles
       // only win when they avoid a large amount of padding
-      double score = eff * useful * (bn == 256 ? 1.0 : bn == 224 ? 0.85 : 0.6);
+      double score = eff * useful * (bn == 256 ? 1.0 : bn == 224 ? 0.85 : 0.6) *
+                     (cg == 1 ? 0.8 : 1.0);
       if (score > best_score) {
         best_score = score;
         best = Cfg{bn, cg, clusters * cg, mblk, nblk, tiles};
@@ -966,7 +976,7 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
       CUDA_TRY(cudaMemsetAsync(p.ws_flags, 0, need - slabs, cs));
     }
   }
-  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
+  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
   p.order[0] = 0;
   p.epoch = 1;
   p.timeout_ns = 5000000000ull;
@@ -1082,7 +1092,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
+  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
@@ -1203,7 +1213,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg);
+  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);

@@ -411,6 +411,73 @@ def test_ragged_shapes_ag_and_rs_exact(rng, world_size, rows, n, k):
             assert np.array_equal(gathered, oracle.gathered_layout(shards))
 
 
+@pytest.mark.parametrize("world_size", [1, 2])
+def test_gemm_rs_fused_and_unfused_calls_interleave(rng, monkeypatch, world_size):
+    # the per-source element counters advance identically with the reduction
+    # fused into the epilogue or run as a separate kernel (SHB_RS_UNFUSED=1),
+    # so the two can alternate on one buffer set without stalls
+    shape = ProblemShape(m=512 * world_size, n=256, k=128, dtype="bfloat16")
+    with make_world(world_size, heap_bytes=1 << 26, timeout_s=5.0) as w:
+        bufs = make_gemm_rs_buffers(w, shape)
+        amats = [ints(rng, -2, 3, (shape.m, shape.k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (shape.k, shape.n))
+        ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+        for mode in ["0", "1", "0", "1", "1", "0"]:
+            monkeypatch.setenv("SHB_RS_UNFUSED", mode)
+
+            def body(pe):
+                a, bb = dev(amats[pe.rank], pe), dev(b, pe)
+                return gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, world_size), bufs,
+                               reset=False)
+
+            for r, y in enumerate(run_np(w, body)):
+                assert np.array_equal(y, ref[r])
+            for r in range(world_size):
+                w.check_errors(r)
+
+
+@pytest.mark.parametrize("cg", [0, 1, 2])  # 0: automatic (1-CTA tiles for chunks <= 128 rows)
+@pytest.mark.parametrize("world_size,rows,n,k", [(8, 128, 512, 256), (4, 128, 384, 136),
+                                                 (2, 384, 264, 200)])
+def test_fused_ops_exact_per_tile_config(rng, world_size, rows, n, k, cg):
+    # TP=8 at M=1024 gives 128-row chunks: the automatic choice switches to
+    # single-CTA tiles there; both fused epilogues must stay bit-exact either way
+    from paper_2504_19442_b200 import _lib
+
+    lib = _lib.load()
+    _lib.check(lib.sh_set_tile_config(0, cg))
+    try:
+        m = rows * world_size
+        shape = ProblemShape(m=m, n=n, k=k, dtype="bfloat16")
+        with make_world(world_size, heap_bytes=1 << 26) as w:
+            agb, rsb = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+            shards = [ints(rng, -2, 3, (rows, k)) for _ in range(world_size)]
+            amats = [ints(rng, -1, 2, (m, k)) for _ in range(world_size)]
+            b = ints(rng, -1, 2, (k, n))
+            ag_ref = oracle.ag_gemm_reference(shards, b)
+            rs_ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+
+            def body(pe):
+                x, a, bb = dev(shards[pe.rank], pe), dev(amats[pe.rank], pe), dev(b, pe)
+                hs = [ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, world_size), agb,
+                              reset=False) for _ in range(2)]
+                ys = [gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, world_size), rsb,
+                              reset=False) for _ in range(2)]
+                return hs, ys
+
+            for r, (hs, ys) in enumerate(run_np(w, body)):
+                for h in hs:
+                    assert np.array_equal(h, ag_ref)
+                for y in ys:
+                    assert np.array_equal(y, rs_ref[r])
+                staging = to_np(w.read_tensor(r, rsb.staging, BF16, (world_size, rows, n)))
+                assert np.array_equal(staging, oracle.staging_layout(amats, [b] * world_size, r))
+                gathered = to_np(w.read_tensor(r, agb.gathered, BF16, (m, k)))
+                assert np.array_equal(gathered, oracle.gathered_layout(shards))
+    finally:
+        lib.sh_set_tile_config(0, 0)
+
+
 def test_unaligned_row_length_rejected():
     # rows must be 16-byte TMA strides: n % 8 / k % 8 != 0 is an ArgumentError,
     # never a silent CPU fallback

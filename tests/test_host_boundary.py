@@ -109,3 +109,21 @@ def test_world_refuses_without_cuda():
 
     with pytest.raises(ConfigurationError, match="no CUDA device"):
         init_world(WorldSpec(world_size=1))
+
+
+def test_tile_choice_small_chunks_use_single_cta_tiles():
+    # host-side tile choice (no GPU needed: 148 SMs assumed): TP=8 at M=1024
+    # gives 128-row chunks, where a 256-row pair tile would be half padding
+    lib = _lib.load()
+    bn, cg, grid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+
+    def query(rows, world, n):
+        assert lib.sh_query_tile_config(rows, world, n, ctypes.byref(bn), ctypes.byref(cg),
+                                        ctypes.byref(grid)) == _lib.SH_OK
+        return bn.value, cg.value, grid.value
+
+    assert query(128, 8, 3584) == (256, 1, 112)   # AG C5 M=1024 TP=8: one wave of 1-CTA tiles
+    assert query(128, 8, 8192)[1] == 1            # RS C5 M=1024 TP=8
+    assert query(1024, 8, 3584)[:2] == (256, 2)   # C3: pair tiles
+    assert query(8192, 1, 3584) == (256, 2, 148)
+    assert query(512, 4, 7168)[1] == 2
