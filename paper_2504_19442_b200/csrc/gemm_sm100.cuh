@@ -72,6 +72,17 @@ struct TileParams {
   float* ws;                          // clusters x (CG*128) x BN fp32 partials
   uint64_t* ws_flags;                 // clusters x CG x 4 epilogue warps
   uint64_t ws_epoch;                  // launch counter of this workspace
+  // Wave lockstep: cluster c runs data-parallel tiles c, c+C, c+2C, ...; the
+  // i-th of them forms wave i.  When K is long, the operand reuse between the
+  // tiles of a wave comes only from their walking K together (a block's
+  // k-slice must still be in L2 when the next tile asks for it), and clusters
+  // drift apart over many waves.  The leader producer publishes
+  // wave_tag | tiles_issued in wave_flags[cluster] and, before issuing wave i,
+  // waits (bounded, a hint -- never an error) until every cluster that has a
+  // wave i-1 tile has issued it.  MMA and epilogue are not gated, so the wait
+  // is absorbed by the smem stages.  null: off.
+  uint64_t* wave_flags;
+  uint64_t wave_tag;
   int* err;                           // host-mapped error word
   uint64_t timeout_ns;
 };
@@ -84,6 +95,27 @@ __device__ __forceinline__ void trace_rec(const TileParams& p, int slot, uint64_
   r[1] = t0;
   r[2] = t1;
   r[3] = tile;
+}
+
+// Warp-wide: wait until every cluster d holding a data-parallel tile of wave
+// i-1 (d + (i-1)*C < dp_tiles) has published >= i issued tiles.  Bounded to
+// 2 ms: the lockstep is a locality hint, a straggler must never stall a call.
+__device__ __forceinline__ void wave_wait(const uint64_t* flags, uint64_t tag, int i, int C,
+                                          int dp_tiles) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t want = tag | (uint64_t)i;
+  const long long first = (long long)(i - 1) * C;
+  uint64_t t0 = 0;
+  for (;;) {
+    bool ok = true;
+    for (int d = (int)lane; d < C; d += 32)
+      if (first + d < dp_tiles && ld_relaxed_gpu(flags + d) < want) ok = false;
+    if (__all_sync(0xffffffffu, ok)) return;
+    const uint64_t now = globaltimer();
+    if (t0 == 0) t0 = now;
+    else if (now - t0 > 2000000ull) return;
+    __nanosleep(64);
+  }
 }
 
 struct WorkItem {
@@ -344,9 +376,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       WorkIter wi;
       wi.init(p, cluster_id, num_clusters, num_kb, ring, leader ? 0 : 1, CG);
       WorkItem w;
+      int waves_issued = 0;  // data-parallel tiles this cluster has issued
+      const bool wave_lead = p.wave_flags != nullptr && leader;
       while (wi.next(w)) {
         int chunk, mb, nb;
         decode_tile(p, w.t, chunk, mb, nb);
+        const bool dp_item = w.t < p.dp_tiles;
+        if (wave_lead && dp_item && waves_issued > 0)
+          wave_wait(p.wave_flags, p.wave_tag, waves_issued, num_clusters, p.dp_tiles);
         const bool own = (MODE == MODE_AG) && chunk == p.rank;
         const bool copying = own && p.copy_own;
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
@@ -416,6 +453,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (wave_lead && dp_item) {
+          ++waves_issued;
+          if (lane == 0) st_relaxed_gpu(p.wave_flags + cluster_id, p.wave_tag | waves_issued);
         }
       }
     }

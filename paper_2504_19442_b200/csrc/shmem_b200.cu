@@ -430,6 +430,22 @@ int zero_counter(int* counter, cudaStream_t s) {
   return SH_OK;
 }
 
+// Wave lockstep of the data-parallel tiles (see TileParams::wave_flags):
+// opt-in (SHB_WAVE=1); not with the dynamic scheduler (no fixed waves).
+// Measured on B200 (RS M=16384 K=28672, one launch under ncu): DRAM reads
+// 15.0 -> 8.1 GB, 5.50 -> 5.15 ms; but in back-to-back power-capped runs
+// the same kernel is 17% slower with it (5.67 -> 6.61 ms median of 5
+// interleaved rounds), and C3/C4 lose 3%, so it stays off by default.
+constexpr int kWaveFlags = 256;
+bool wave_sync_on() { return env_int("SHB_WAVE", 0) != 0; }
+
+template <typename RS>
+void attach_wave(RS& rs, TileParams& p) {
+  if (!wave_sync_on() || p.tile_counter || !rs.wave) return;
+  p.wave_flags = rs.wave;
+  p.wave_tag = (++rs.wave_epoch) << 32;
+}
+
 template <typename RS>
 void attach_trace(RS& rs, TileParams& p, int mode) {
   if (!rs.trace) return;
@@ -474,6 +490,8 @@ struct RankState {
   int ranks_on_device = 1;  // ranks of this process on `device` (incl. this one)
   SkWorkspace sk;           // stream-K partials of this rank's AG launches
   int* tile_counter = nullptr;  // dynamic tile scheduler counter (zeroed per launch)
+  uint64_t* wave = nullptr;     // per-cluster wave progress flags (epoch-tagged)
+  uint64_t wave_epoch = 0;
   uint64_t* trace = nullptr;  // [max_launches][grid_max][cap][4] timeline records
   int trace_cap = 0, trace_launches = 0, trace_grid = 0;
   long long trace_count = 0;  // launches recorded so far
@@ -503,6 +521,8 @@ int init_rank_common(sh_world* w, RankState& rs) {
   if ((rc = sk_reserve(rs.sk, num_sms(rs.device) / 2, 2, 256))) return rc;
   CUDA_TRY(cudaMalloc(&rs.tile_counter, 256));
   CUDA_TRY(cudaMemset(rs.tile_counter, 0, 256));
+  CUDA_TRY(cudaMalloc(&rs.wave, kWaveFlags * sizeof(uint64_t)));
+  CUDA_TRY(cudaMemset(rs.wave, 0, kWaveFlags * sizeof(uint64_t)));
   CUDA_TRY(cudaStreamCreateWithFlags(&rs.comm, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_in, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&rs.ev_done, cudaEventDisableTiming));
@@ -728,6 +748,7 @@ int sh_world_destroy(sh_world* w) {
     if (rs.err_host) cudaFreeHost(rs.err_host);
     if (rs.trace) cudaFree(rs.trace);
     if (rs.tile_counter) cudaFree(rs.tile_counter);
+    if (rs.wave) cudaFree(rs.wave);
     if (rs.sk.ws) cudaFree(rs.sk.ws);
     if (rs.sk.flags) cudaFree(rs.sk.flags);
   }
@@ -901,7 +922,9 @@ size_t sk_workspace_bytes(const Cfg& c) {
   return clusters * c.cg * 128 * (size_t)c.bn * sizeof(float) + clusters * c.cg * 4 * 8;
 }
 
-constexpr size_t kCounterBytes = 256;  // dynamic tile counter at the front of the workspace
+// front of the caller's workspace: dynamic tile counter (256 B), then the
+// wave progress flags (kWaveFlags u64)
+constexpr size_t kCounterBytes = 256 + kWaveFlags * sizeof(uint64_t);
 
 int sh_gemm_workspace_bytes(int m, int n, int k, size_t* bytes) {
   if (!bytes) return fail(SH_ERR_ARG, "null argument");
@@ -962,6 +985,11 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   if (have_ws && dynamic_tiles()) {
     p.tile_counter = static_cast<int*>(workspace);
     if ((rc = zero_counter(p.tile_counter, cs))) return rc;
+  }
+  if (have_ws && !p.tile_counter && wave_sync_on()) {
+    p.wave_flags = reinterpret_cast<uint64_t*>(static_cast<char*>(workspace) + 256);
+    p.wave_tag = 1ull << 32;
+    CUDA_TRY(cudaMemsetAsync(p.wave_flags, 0, kWaveFlags * sizeof(uint64_t), cs));
   }
   if (p.dp_tiles < p.num_tiles) {
     const size_t need = sk_workspace_bytes(cfg);
@@ -1101,6 +1129,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     p.tile_counter = rs->tile_counter;
     if ((rc = zero_counter(rs->tile_counter, s))) return rc;
   }
+  attach_wave(*rs, p);
   p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
   if (p.dp_tiles < p.num_tiles) {
     if ((rc = sk_reserve(rs->sk, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
@@ -1222,12 +1251,32 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
       reinterpret_cast<const uint16_t*>(static_cast<char*>(rs->peer[rank]) + staging_off);
   const size_t slot_elems = (size_t)rows * n;
   const uint64_t target = epoch * (uint64_t)slot_elems;
-  p.dp_tiles = p.num_tiles;  // RS tiles publish per chunk; no stream-K split
+  // Stream-K tail as in the AG GEMM.  A cluster's stream-K pieces come after
+  // its data-parallel tiles; with the reduction fused, an own-chunk tile
+  // waits for every peer's contribution, so a peer-chunk piece queued behind
+  // it could close a wait cycle across ranks.  The split is therefore only
+  // taken when the whole stream-K range lies inside my own chunk, scheduled
+  // last (rs_inter_order), or when nothing waits on peers.
+  p.dp_tiles = p.num_tiles;
+  {
+    const int dp = stream_k_split(cfg, (k + 63) / 64);
+    const int per_chunk = cfg.mblk * cfg.nblk;
+    const bool safe = !fuse || W == 1 ||
+                      (chunk_order[W - 1] == rank && p.num_tiles - dp <= per_chunk);
+    if (dp < p.num_tiles && safe) {
+      if ((rc = sk_reserve(rs->sk, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
+      p.dp_tiles = dp;
+      p.ws = rs->sk.ws;
+      p.ws_flags = rs->sk.flags;
+      p.ws_epoch = ++rs->sk.epoch;
+    }
+  }
   attach_trace(*rs, p, MODE_RS);
   if (dynamic_tiles()) {
     p.tile_counter = rs->tile_counter;
     if ((rc = zero_counter(rs->tile_counter, s))) return rc;
   }
+  attach_wave(*rs, p);
   p.rs_mine = sig_addr(w, *rs, rank, reduction_base);
   p.rs_target = target;
   p.staging_local = staging;

@@ -358,10 +358,11 @@ def test_ag_gemm_stream_k_tail_exact(rng, monkeypatch, world_size, dyn):
 @pytest.mark.parametrize("world_size", [1, 2])
 def test_gemm_rs_stream_k_tail_exact(rng, monkeypatch, world_size, dyn):
     # the fused RS epilogue behind stream-K partial tiles: finishers publish
-    # the summed tile into the peers' staging slots
+    # the summed tile into the peers' staging slots (W=2: 160 tiles on 37
+    # clusters per rank, the 49-tile stream-K range inside the own chunk)
     monkeypatch.setenv("SHB_SK", "1")
     monkeypatch.setenv("SHB_DYN", dyn)
-    shape = ProblemShape(m=2560, n=2048, k=512, dtype="bfloat16")
+    shape = ProblemShape(m=2560 * world_size, n=2048, k=512, dtype="bfloat16")
     with make_world(world_size, heap_bytes=1 << 26) as w:
         bufs = make_gemm_rs_buffers(w, shape)
         amats = [ints(rng, -2, 3, (shape.m, shape.k)) for _ in range(world_size)]
