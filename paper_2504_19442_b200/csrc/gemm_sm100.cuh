@@ -797,8 +797,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             // nobody waits on my own chunk's counter in the fused path, but it
             // advances all the same, so the counters mean the same thing in
-            // both modes (a later unfused call targets epoch * rows * n)
-            red_add_release_sys(p.rs_count[chunk], (uint64_t)vr * (uint64_t)vc);
+            // both modes (a later unfused call targets epoch * rows * n, and
+            // is stream-ordered after this kernel: no release fence needed)
+            red_add_relaxed_gpu(p.rs_count[chunk], (uint64_t)vr * (uint64_t)vc);
           }
         }
         __syncwarp();
