@@ -77,11 +77,13 @@ def test_gemm_stream_k_tail(monkeypatch, sk, m, n, k):
     assert rel_fro(c, a.float() @ b.float()) < TOL
 
 
-@pytest.mark.parametrize("dyn", ["0", "1"])
-def test_gemm_stream_k_exact_integers(monkeypatch, dyn):
-    # dyn=1: data-parallel tiles handed out by the atomic counter (opt-in)
+@pytest.mark.parametrize("dyn,wave", [("0", "0"), ("1", "0"), ("0", "1")])
+def test_gemm_stream_k_exact_integers(monkeypatch, dyn, wave):
+    # dyn=1: data-parallel tiles handed out by the atomic counter (opt-in);
+    # wave=1: wave lockstep of the data-parallel tiles (opt-in)
     monkeypatch.setenv("SHB_SK", "1")
     monkeypatch.setenv("SHB_DYN", dyn)
+    monkeypatch.setenv("SHB_WAVE", wave)
     g = torch.Generator(device="cuda").manual_seed(3)
     a = torch.randint(-2, 3, (2560, 1024), device="cuda", generator=g).to(torch.bfloat16)
     b = torch.randint(-1, 2, (1024, 2048), device="cuda", generator=g).to(torch.bfloat16)

@@ -535,3 +535,33 @@ def test_criterion_6_pipeline_correctness_on_gpu():
             for other in outs[1:]:  # bit-identical across schedules
                 for (h0, y0), (h1, y1) in zip(outs[0], other):
                     assert np.array_equal(h0, h1) and np.array_equal(y0, y1)
+
+
+@pytest.mark.parametrize("world_size", [1, 2])
+def test_wave_lockstep_exact(rng, monkeypatch, world_size):
+    # opt-in wave lockstep (SHB_WAVE=1) of the data-parallel tiles: several
+    # waves per rank, both fused ops, back-to-back calls (epoch-tagged flags)
+    monkeypatch.setenv("SHB_WAVE", "1")
+    shape = ProblemShape(m=4096 * world_size, n=2048, k=256, dtype="bfloat16")
+    rows = shape.m // world_size
+    with make_world(world_size, heap_bytes=1 << 27) as w:
+        agb, rsb = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (rows, shape.k)) for _ in range(world_size)]
+        amats = [ints(rng, -1, 2, (shape.m, shape.k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (shape.k, shape.n))
+        ag_ref = oracle.ag_gemm_reference(shards, b)
+        rs_ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+
+        def body(pe):
+            x, a, bb = dev(shards[pe.rank], pe), dev(amats[pe.rank], pe), dev(b, pe)
+            hs = [ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, world_size), agb,
+                          reset=False) for _ in range(3)]
+            ys = [gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, world_size), rsb,
+                          reset=False) for _ in range(3)]
+            return hs, ys
+
+        for r, (hs, ys) in enumerate(run_np(w, body)):
+            for h in hs:
+                assert np.array_equal(h, ag_ref)
+            for y in ys:
+                assert np.array_equal(y, rs_ref[r])
