@@ -132,6 +132,23 @@ int sh_signal_wait(sh_world* w, int rank, int sig, int cond, uint64_t value, voi
 int sh_reduce_slots(sh_world* w, int rank, size_t staging_off, int nslots, size_t slot_elems,
                     int dtype, void* out, void* stream);
 
+/* Node-scope multimem (reference Pe.multimem_st / Pe.multimem_ld_reduce,
+ * primitives.py:291-315), over the node's ranks [first, first + count):
+ * sh_multimem_st replicates the caller's bytes [offset, offset + nbytes) of
+ * its own replica into every other node rank's replica (one read, count-1
+ * NVLink stores per 16 B); sh_multimem_ld_reduce writes into the device
+ * buffer `out` the element-wise sum of the node's replicas in ascending rank
+ * order, computed like numpy's `out += replica` in the element type (floats
+ * round per step, integers wrap).  dtype: SH_DTYPE_BF16, FP16, FP32, I32,
+ * I64, U8, I8; nbytes must be a multiple of the element size.  Both are
+ * stream-ordered: the caller orders them after the peers' writes (barrier). */
+#define SH_DTYPE_U8 5
+#define SH_DTYPE_I8 6
+int sh_multimem_st(sh_world* w, int rank, int first, int count, size_t offset, size_t nbytes,
+                   void* stream);
+int sh_multimem_ld_reduce(sh_world* w, int rank, int first, int count, size_t offset,
+                          size_t nbytes, int dtype, void* out, void* stream);
+
 /* Timeline evidence (reference World.start_trace/stop_trace, core.py:434-444,
  * and Timeline.to_chrome_trace, costmodel.py:185-190): while enabled, every
  * fused launch of `rank` records %globaltimer stamps per CTA -- chunk-flag

@@ -85,6 +85,11 @@ SIGNATURES = {
                                       ctypes.c_uint64, _vp]),
     "sh_reduce_slots": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_size_t, ctypes.c_int,
                                        ctypes.c_size_t, ctypes.c_int, _vp, _vp]),
+    "sh_multimem_st": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_size_t, ctypes.c_size_t, _vp]),
+    "sh_multimem_ld_reduce": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int, _vp,
+                                             _vp]),
     "sh_trace_enable": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "sh_trace_read": (ctypes.c_int, [_vp, ctypes.c_int, _c_u64_p, ctypes.c_size_t, _c_int_p]),
     "sh_gemm_workspace_bytes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -250,6 +250,42 @@ class Pe:
         torch.cuda.current_stream(self.device).synchronize()
         return self.world.sig_read(self.rank, sig)
 
+    # ------------------------------------------------------------------
+    # node-scope multimem (reference primitives.py:291-315)
+
+    def _node_range(self):
+        lws = self.world.local_world_size
+        return self.ctx.node_id * lws, lws
+
+    def multimem_st(self, handle: SymHandle, off=0, nbytes=None):
+        """Replicate the caller's bytes at ``handle`` into every same-node
+        rank's replica (SM-driven NVLink stores, one read of the source)."""
+        n = handle.length - off if nbytes is None else nbytes
+        handle.check(off, n)
+        self.world.bump(self.rank, "multimem_st")
+        first, count = self._node_range()
+        _lib.check(self.world._lib.sh_multimem_st(self.world.handle, self.rank, first, count,
+                                                  handle.offset + off, n, self._stream_handle()))
+
+    def multimem_ld_reduce(self, handle: SymHandle, dtype, off=0, nbytes=None):
+        """Element-wise sum of all same-node replicas (ascending rank order,
+        numpy ``out += replica`` arithmetic), as a new CUDA tensor."""
+        import torch
+
+        tdt, code = _multimem_dtype(dtype)
+        esize = torch.empty((), dtype=tdt).element_size()
+        n = handle.length - off if nbytes is None else nbytes
+        handle.check(off, n)
+        if n % esize:
+            raise ArgumentError(f"{n} bytes not a multiple of {esize}-byte elements")
+        self.world.bump(self.rank, "multimem_ld_reduce")
+        out = torch.empty(n // esize, dtype=tdt, device=self.torch_device)
+        first, count = self._node_range()
+        _lib.check(self.world._lib.sh_multimem_ld_reduce(
+            self.world.handle, self.rank, first, count, handle.offset + off, n, code,
+            out.data_ptr(), self._stream_handle()))
+        return out
+
     def local_view(self, handle: SymHandle, dtype=None, shape=None):
         """Zero-copy CUDA view of this rank's replica of ``handle``."""
         import torch
@@ -261,6 +297,27 @@ class Pe:
 
     def __repr__(self):
         return f"Pe(rank={self.rank}, device=cuda:{self.device})"
+
+
+def _multimem_dtype(dtype):
+    """(torch dtype, SH_DTYPE code) for a numpy / torch / string dtype."""
+    import numpy as np
+    import torch
+
+    table = {torch.bfloat16: (torch.bfloat16, 0), torch.float16: (torch.float16, 1),
+             torch.float32: (torch.float32, 2), torch.int32: (torch.int32, 3),
+             torch.int64: (torch.int64, 4), torch.uint8: (torch.uint8, 5),
+             torch.int8: (torch.int8, 6)}
+    if isinstance(dtype, torch.dtype):
+        key = dtype
+    else:
+        name = str(dtype) if isinstance(dtype, str) else np.dtype(dtype).name
+        key = {"bfloat16": torch.bfloat16, "float16": torch.float16, "float32": torch.float32,
+               "int32": torch.int32, "int64": torch.int64, "uint8": torch.uint8,
+               "int8": torch.int8}.get(name)
+    if key not in table:
+        raise ArgumentError(f"multimem_ld_reduce does not support dtype {dtype}")
+    return table[key]
 
 
 class _HostBarrier:

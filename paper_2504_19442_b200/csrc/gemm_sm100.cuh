@@ -902,6 +902,88 @@ __global__ void __launch_bounds__(256) slots_reduce_kernel(const T* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Node-scope multimem (reference primitives.py:291-315).  The symmetric slabs
+// of the node's ranks are mapped into this rank's address space (peer access
+// / CUDA IPC), so both are SM-driven NVLink transfers: multimem_st reads the
+// caller's bytes once and stores them into every other replica (P2P stores),
+// multimem_ld_reduce loads every replica (P2P loads) and sums them in
+// ascending rank order with numpy's `out += replica` arithmetic: the sum
+// starts from +0 and every step rounds to the element type (floats) or wraps
+// (integers).
+
+struct PeerList {
+  uint8_t* p[kMaxWorld];
+};
+
+struct AddBF16 {
+  using S = uint16_t;
+  __device__ static S add(S a, S b) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(__bfloat162float(__ushort_as_bfloat16(a)) +
+                                                    __bfloat162float(__ushort_as_bfloat16(b))));
+  }
+};
+struct AddFP16 {
+  using S = uint16_t;
+  __device__ static S add(S a, S b) {
+    return __half_as_ushort(
+        __float2half_rn(__half2float(__ushort_as_half(a)) + __half2float(__ushort_as_half(b))));
+  }
+};
+struct AddF32 {
+  using S = float;
+  __device__ static S add(S a, S b) { return a + b; }
+};
+template <typename T, typename U>
+struct AddWrap {  // two's-complement wrap-around through the unsigned type
+  using S = T;
+  __device__ static S add(S a, S b) { return (S)(U)((U)a + (U)b); }
+};
+
+template <typename Op>
+__global__ void __launch_bounds__(256) peers_reduce_kernel(const __grid_constant__ PeerList src,
+                                                           int npeers, typename Op::S* out,
+                                                           size_t elems, int vec) {
+  using S = typename Op::S;
+  constexpr int E = 16 / sizeof(S);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t nvec = vec ? elems / E : 0;
+  for (size_t i = tid; i < nvec; i += stride) {
+    S acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = S(0);
+    for (int r = 0; r < npeers; ++r) {
+      const uint4 w = reinterpret_cast<const uint4*>(src.p[r])[i];
+      const S* x = reinterpret_cast<const S*>(&w);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = Op::add(acc[e], x[e]);
+    }
+    reinterpret_cast<uint4*>(out)[i] = *reinterpret_cast<const uint4*>(acc);
+  }
+  for (size_t i = nvec * E + tid; i < elems; i += stride) {
+    S acc = S(0);
+    for (int r = 0; r < npeers; ++r) acc = Op::add(acc, reinterpret_cast<const S*>(src.p[r])[i]);
+    out[i] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) multimem_st_kernel(const __grid_constant__ PeerList dst,
+                                                          int ndst, const uint8_t* src,
+                                                          size_t nbytes, int vec) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t nvec = vec ? nbytes / 16 : 0;
+  for (size_t i = tid; i < nvec; i += stride) {
+    const uint4 v = reinterpret_cast<const uint4*>(src)[i];
+    for (int d = 0; d < ndst; ++d) reinterpret_cast<uint4*>(dst.p[d])[i] = v;
+  }
+  for (size_t i = nvec * 16 + tid; i < nbytes; i += stride) {
+    const uint8_t v = src[i];
+    for (int d = 0; d < ndst; ++d) dst.p[d][i] = v;
+  }
+}
+
 // Bounded spin for the wait conditions the front end cannot evaluate.
 __global__ void flag_wait_cond_kernel(const uint64_t* flag, int cond, uint64_t value, int* err,
                                       uint64_t timeout_ns) {

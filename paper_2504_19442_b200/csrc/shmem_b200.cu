@@ -373,6 +373,15 @@ int preload_kernels(int dev) {
                          reinterpret_cast<const void*>(slots_reduce_kernel<float, float>),
                          reinterpret_cast<const void*>(slots_reduce_kernel<int32_t, int32_t>),
                          reinterpret_cast<const void*>(slots_reduce_kernel<long long, long long>),
+                         reinterpret_cast<const void*>(peers_reduce_kernel<AddBF16>),
+                         reinterpret_cast<const void*>(peers_reduce_kernel<AddFP16>),
+                         reinterpret_cast<const void*>(peers_reduce_kernel<AddF32>),
+                         reinterpret_cast<const void*>(peers_reduce_kernel<AddWrap<int32_t, uint32_t>>),
+                         reinterpret_cast<const void*>(
+                             peers_reduce_kernel<AddWrap<long long, unsigned long long>>),
+                         reinterpret_cast<const void*>(peers_reduce_kernel<AddWrap<uint8_t, uint8_t>>),
+                         reinterpret_cast<const void*>(peers_reduce_kernel<AddWrap<int8_t, uint8_t>>),
+                         reinterpret_cast<const void*>(multimem_st_kernel),
                          reinterpret_cast<const void*>(flag_wait_cond_kernel),
                          reinterpret_cast<const void*>(flag_add_kernel),
                          reinterpret_cast<const void*>(rs_reduce_kernel<false>),
@@ -1422,6 +1431,107 @@ int sh_reduce_slots(sh_world* w, int rank, size_t staging_off, int nslots, size_
     default:
       slots_reduce_kernel<long long, long long><<<grid, 256, 0, s>>>(
           static_cast<const long long*>(st), static_cast<long long*>(out), slot_elems, nslots);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+namespace {
+
+int node_peers(sh_world* w, RankState* rs, int rank, int first, int count, size_t offset,
+               size_t nbytes, PeerList& pl, int& n, bool skip_self) {
+  if (first < 0 || count < 1 || first + count > w->world || rank < first || rank >= first + count)
+    return fail(SH_ERR_ARG, "node ranks [%d, %d) do not hold rank %d (world %d)", first,
+                first + count, rank, w->world);
+  if (offset + nbytes > w->heap_bytes || offset + nbytes < offset)
+    return fail(SH_ERR_ARG, "range [%zu, %zu) outside heap of %zu", offset, offset + nbytes,
+                w->heap_bytes);
+  n = 0;
+  for (int q = first; q < first + count; ++q) {
+    if (skip_self && q == rank) continue;
+    if (!rs->peer[q]) return fail(SH_ERR_ARG, "rank %d has no mapping of rank %d", rank, q);
+    pl.p[n++] = static_cast<uint8_t*>(rs->peer[q]) + offset;
+  }
+  return SH_OK;
+}
+
+bool all16(const PeerList& pl, int n, const void* extra) {
+  for (int i = 0; i < n; ++i)
+    if (reinterpret_cast<uintptr_t>(pl.p[i]) & 15) return false;
+  return (reinterpret_cast<uintptr_t>(extra) & 15) == 0;
+}
+
+}  // namespace
+
+int sh_multimem_st(sh_world* w, int rank, int first, int count, size_t offset, size_t nbytes,
+                   void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  PeerList pl;
+  memset(&pl, 0, sizeof(pl));
+  int n = 0;
+  int rc = node_peers(w, rs, rank, first, count, offset, nbytes, pl, n, true);
+  if (rc) return rc;
+  if (nbytes == 0 || n == 0) return SH_OK;
+  CUDA_TRY(cudaSetDevice(rs->device));
+  const uint8_t* src = static_cast<const uint8_t*>(rs->peer[rank]) + offset;
+  const int vec = all16(pl, n, src) ? 1 : 0;
+  const size_t work = vec ? nbytes / 16 + 1 : nbytes;
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>((work + 255) / 256,
+                                                             (size_t)num_sms(rs->device) * 4));
+  multimem_st_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(pl, n, src, nbytes,
+                                                                          vec);
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_multimem_ld_reduce(sh_world* w, int rank, int first, int count, size_t offset,
+                          size_t nbytes, int dtype, void* out, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  static const size_t esize[] = {2, 2, 4, 4, 8, 1, 1};
+  if (dtype < 0 || dtype > SH_DTYPE_I8) return fail(SH_ERR_ARG, "dtype %d not supported", dtype);
+  if (nbytes % esize[dtype])
+    return fail(SH_ERR_ARG, "%zu bytes not a multiple of %zu-byte elements", nbytes, esize[dtype]);
+  PeerList pl;
+  memset(&pl, 0, sizeof(pl));
+  int n = 0;
+  int rc = node_peers(w, rs, rank, first, count, offset, nbytes, pl, n, false);
+  if (rc) return rc;
+  if (nbytes == 0) return SH_OK;
+  if (!out) return fail(SH_ERR_ARG, "null output");
+  CUDA_TRY(cudaSetDevice(rs->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t elems = nbytes / esize[dtype];
+  const int vec = all16(pl, n, out) ? 1 : 0;
+  const size_t work = vec ? nbytes / 16 + 1 : elems;
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>((work + 255) / 256,
+                                                             (size_t)num_sms(rs->device) * 4));
+  switch (dtype) {
+    case SH_DTYPE_BF16:
+      peers_reduce_kernel<AddBF16><<<grid, 256, 0, s>>>(pl, n, static_cast<uint16_t*>(out), elems, vec);
+      break;
+    case SH_DTYPE_FP16:
+      peers_reduce_kernel<AddFP16><<<grid, 256, 0, s>>>(pl, n, static_cast<uint16_t*>(out), elems, vec);
+      break;
+    case SH_DTYPE_FP32:
+      peers_reduce_kernel<AddF32><<<grid, 256, 0, s>>>(pl, n, static_cast<float*>(out), elems, vec);
+      break;
+    case SH_DTYPE_I32:
+      peers_reduce_kernel<AddWrap<int32_t, uint32_t>><<<grid, 256, 0, s>>>(
+          pl, n, static_cast<int32_t*>(out), elems, vec);
+      break;
+    case SH_DTYPE_I64:
+      peers_reduce_kernel<AddWrap<long long, unsigned long long>><<<grid, 256, 0, s>>>(
+          pl, n, static_cast<long long*>(out), elems, vec);
+      break;
+    case SH_DTYPE_U8:
+      peers_reduce_kernel<AddWrap<uint8_t, uint8_t>><<<grid, 256, 0, s>>>(
+          pl, n, static_cast<uint8_t*>(out), elems, vec);
+      break;
+    default:
+      peers_reduce_kernel<AddWrap<int8_t, uint8_t>><<<grid, 256, 0, s>>>(
+          pl, n, static_cast<int8_t*>(out), elems, vec);
   }
   CUDA_TRY(cudaGetLastError());
   return SH_OK;

@@ -218,3 +218,120 @@ def test_world_copy_into_and_read_from():
         w.copy_into(1, h, 4, b"abcdefgh")
         assert w.read_from(1, h, 4, 8) == b"abcdefgh"
         assert w.read_from(0, h, 0, 16) == bytes(16)
+
+
+# ---------------------------------------------------------------------------
+# node-scope multimem (reference tests/test_primitives.py:211-256)
+
+def test_multimem_st_broadcasts_within_node():
+    # one NVSwitch node (multi-node worlds are out of scope): every rank's
+    # replica receives rank 1's bytes, the other ranks' zeros are overwritten
+    with make_world(4, heap_bytes=1 << 10) as w:
+        h = w.alloc_symmetric(16)
+
+        def body(pe):
+            if pe.rank == 1:
+                pe.putmem(h, b"n" * 16, pe.rank)
+                pe.multimem_st(h)
+            pe.barrier_all()
+            return view_bytes(pe, h)
+
+        res = [as_bytes(t) for t in w.run(body)]
+        assert all(r == b"n" * 16 for r in res)
+        assert w.counters(1).get("multimem_st") == 1
+        assert w.counters(0).get("multimem_st", 0) == 0
+
+
+def test_multimem_ld_reduce_sums_node():
+    with make_world(4, heap_bytes=1 << 10) as w:
+        h = w.alloc_symmetric(16)
+
+        def body(pe):
+            vals = np.full(2, pe.rank + 1, dtype=np.int64)
+            pe.putmem(h, vals.tobytes(), pe.rank)
+            pe.barrier_all()
+            return pe.multimem_ld_reduce(h, np.int64)
+
+        for got in w.run(body):
+            assert got.cpu().tolist() == [10, 10]  # 1+2+3+4
+        with pytest.raises(CollectiveFault) as info:
+            w.run(lambda pe: pe.multimem_ld_reduce(h, np.int64, nbytes=12))
+        assert isinstance(info.value.first, ArgumentError)
+
+
+def test_multimem_single_rank_node_identity():
+    # a node of one rank: multimem_st is a no-op, ld_reduce returns the replica
+    with make_world(1, heap_bytes=1 << 10) as w:
+        h = w.alloc_symmetric(8)
+
+        def body(pe):
+            pe.putmem(h, bytes([pe.rank + 1] * 8), pe.rank)
+            pe.multimem_st(h)
+            return pe.multimem_ld_reduce(h, np.uint8)
+
+        assert [t.cpu().tolist() for t in w.run(body)] == [[1] * 8]
+
+
+@pytest.mark.parametrize("dtype", ["bfloat16", "float16", "float32", "int32", "int64", "uint8",
+                                   "int8"])
+@pytest.mark.parametrize("nbytes_extra", [0, 8])  # 16-B vector path and the scalar tail
+def test_multimem_ld_reduce_matches_numpy_accumulation(rng, dtype, nbytes_extra):
+    # the per-step arithmetic of the reference's `out += replica` (floats round
+    # to the element type after every add, integers wrap), ascending ranks
+    import ml_dtypes  # noqa: F401  (numpy bfloat16)
+
+    W = 4
+    npdt = np.dtype("bfloat16" if dtype == "bfloat16" else dtype)
+    elems = (4096 + nbytes_extra) // npdt.itemsize
+    if np.issubdtype(npdt, np.integer):
+        info = np.iinfo(npdt)
+        reps = [rng.integers(info.min, info.max, elems, endpoint=True).astype(npdt)
+                for _ in range(W)]
+    else:
+        reps = [(rng.standard_normal(elems) * 100).astype(np.float32).astype(npdt)
+                for _ in range(W)]
+    expect = np.zeros(elems, dtype=npdt)
+    with np.errstate(over="ignore"):
+        for r in reps:
+            expect += r
+    with make_world(W, heap_bytes=1 << 16) as w:
+        h = w.alloc_symmetric(reps[0].nbytes, align=16)
+
+        def body(pe):
+            pe.putmem(h, reps[pe.rank].tobytes(), pe.rank)
+            pe.barrier_all()
+            return pe.multimem_ld_reduce(h, dtype)
+
+        for got in w.run(body):
+            g = got.cpu()
+            if dtype == "bfloat16":
+                g = g.view(torch.int16).numpy().view(np.uint16)
+                e = expect.view(np.uint16)
+            else:
+                g, e = g.numpy(), expect
+            assert g.tobytes() == e.tobytes()
+
+
+def test_multimem_st_large_unaligned_range(rng):
+    # a range that is neither 16-B aligned nor a multiple of 16 B takes the
+    # byte path; a large aligned one the vector path
+    W = 3
+    with make_world(W, heap_bytes=1 << 21) as w:
+        h = w.alloc_symmetric(1 << 20, align=256)
+        data = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+
+        def body(pe):
+            if pe.rank == 2:
+                pe.putmem(h, data.tobytes(), pe.rank)
+                pe.multimem_st(h, off=0, nbytes=(1 << 19))        # vector path
+                pe.multimem_st(h, off=(1 << 19) + 3, nbytes=1001)  # byte path
+            pe.barrier_all()
+            return view_bytes(pe, h)
+
+        res = [t.cpu().numpy() for t in w.run(body)]
+        for r in range(W):
+            assert np.array_equal(res[r][:1 << 19], data[:1 << 19])
+            lo = (1 << 19) + 3
+            assert np.array_equal(res[r][lo:lo + 1001], data[lo:lo + 1001])
+            if r != 2:
+                assert not res[r][lo + 1001:].any() and not res[r][(1 << 19):lo].any()
