@@ -405,10 +405,40 @@ def main():
                 u1.record(stream)
                 barrier()
                 ums = max_over_ranks(u0.elapsed_time(u1) / ku)
+
+                # the two K-step blocks above run minutes apart in different
+                # power states (1 kW cap); an interleaved A/B with alternating
+                # order is the apples-to-apples comparison
+                def block(fn, n):
+                    b0, b1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                    barrier()
+                    b0.record(stream)
+                    for _ in range(n):
+                        fn()
+                    b1.record(stream)
+                    barrier()
+                    return max_over_ranks(b0.elapsed_time(b1) / n)
+
+                ab_steps, ab_rounds = 100, 6
+                ab = {"ours": [], "unfused": []}
+                for r in range(ab_rounds):
+                    order = [("ours", lambda: step(x)), ("unfused", ustep)]
+                    for name, fn in (order if r % 2 == 0 else order[::-1]):
+                        ab[name].append(block(fn, ab_steps))
+                o_ms = statistics.median(ab["ours"])
+                u_ms = statistics.median(ab["unfused"])
             unfused = {"impl": "torch.matmul (cuBLASLt)" + (" + NCCL all_gather/reduce_scatter"
                                                             if N > 1 else ""),
                        "value": STEP_FLOPS * N / (ums * 1e-3) / 1e12, "unit": "TFLOPS",
-                       "ms_per_step": ums}
+                       "ms_per_step": ums,
+                       "interleaved": {
+                           "rounds": ab_rounds, "steps_per_block": ab_steps,
+                           "ours_ms_per_step": o_ms, "unfused_ms_per_step": u_ms,
+                           "ours_tflops": STEP_FLOPS * N / (o_ms * 1e-3) / 1e12,
+                           "unfused_tflops": STEP_FLOPS * N / (u_ms * 1e-3) / 1e12,
+                           "speedup": u_ms / o_ms,
+                           "how": "median over blocks of 100 back-to-back steps, ours and "
+                                  "unfused alternating (order flipped every round)"}}
         except Exception as e:  # noqa: BLE001 -- e.g. gloo has no CUDA all_gather
             unfused = {"error": f"{type(e).__name__}: {e}"[:300]}
 
