@@ -143,6 +143,35 @@ class Pe:
         self.world.bump(self.rank, "barrier_all")
         self.world._barrier(self)
 
+    def sync_all(self):
+        """Barrier without the completion reading of the reference (core.py:
+        sync_all); on the GPU the drain makes both the same."""
+        self.world.bump(self.rank, "sync_all")
+        self.world._barrier(self)
+
+    def quiet(self):
+        """Complete this rank's outstanding transfers (reference primitives.py
+        quiet): every put/get is stream-ordered, so drain the current stream."""
+        import torch
+
+        self.world.bump(self.rank, "quiet")
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def my_pe(self):
+        return self.rank
+
+    def n_pes(self):
+        return self.world.world_size
+
+    def remote_ptr(self, handle: SymHandle, peer, off=0, nbytes=None):
+        """Zero-copy CUDA uint8 view of ``peer``'s replica of ``handle``, mapped
+        into this rank's GPU (NVLink loads/stores; reference remote_ptr)."""
+        import torch
+
+        self._check_peer(peer)
+        n = handle.length - off if nbytes is None else nbytes
+        return self.world.heap_view(self.rank, handle, torch.uint8, (n,), off=off, peer=peer)
+
     # ------------------------------------------------------------------
     # one-sided primitives (reference primitives.py:126-257), stream-ordered
 
@@ -188,6 +217,23 @@ class Pe:
                                              dst.offset + dst_off, payload.data_ptr(),
                                              payload.numel(), self._stream_handle()))
         return payload  # keep alive until the caller's stream passes the copy
+
+    def putmem_signal(self, dst: SymHandle, src, sig, value, peer, *, op=None, nbytes=None,
+                      dst_off=0, src_off=0):
+        """putmem followed by a signal on ``peer`` that is ordered after the data
+        (same stream; the stream write carries a memory barrier)."""
+        from .primitives import SignalOp
+
+        keep = self.putmem(dst, src, peer, nbytes=nbytes, dst_off=dst_off, src_off=src_off)
+        self.signal_op(peer, sig, op or SignalOp.SET, value)
+        return keep
+
+    def putmem_nbi(self, dst: SymHandle, src, peer, **kw):
+        """Non-blocking put: every put is already stream-ordered and asynchronous."""
+        return self.putmem(dst, src, peer, **kw)
+
+    def getmem_nbi(self, dst, src: SymHandle, peer, **kw):
+        return self.getmem(dst, src, peer, **kw)
 
     def getmem(self, dst, src: SymHandle, peer, *, nbytes=None, dst_off=0, src_off=0):
         """Copy ``peer``'s replica of ``src`` into ``dst`` (a CUDA tensor or the
