@@ -53,7 +53,8 @@ struct TileParams {
   // (%globaltimer ns); producer records fill from the front, epilogue (warp 2)
   // records from the middle.  Kinds: 1 chunk-flag wait (AG), 2 tile
   // epilogue (t0 = accumulator ready, t1 = stores issued), 3 peer-arrival
-  // wait (fused RS), 4 CTA lifetime.
+  // wait (fused RS), 4 CTA lifetime, 5 MMA accumulator wait (aux = summed
+  // operand-stage waits of the item, ns; MMA warp, last quarter of the slots).
   uint64_t* trace;
   int trace_cap;
   uint64_t l2_hint_a, l2_hint_b;      // TMA L2 cache policies of the operand loads
@@ -474,17 +475,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t b_desc0 = umma_desc(smem_u32(sB), 64 * BK * 2, 1024, 2);
       uint32_t stage = 0, phase = 0;
       int it = 0;
+      // optional timeline (kind 5, last quarter of the CTA's records): per
+      // work item, the wait for a free accumulator [t0, t1) and the summed
+      // time spent waiting for operand stages (aux, ns)
+      const bool mtrace = p.trace != nullptr && lane == 0;
+      int mslot = p.trace_cap * 3 / 4;
       WorkIter wi;
       wi.init(p, cluster_id, num_clusters, num_kb, ring, 1, CG);
       WorkItem w;
       for (; wi.next(w); ++it) {
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
+        const uint64_t tw0 = mtrace ? globaltimer() : 0;
         mbar_wait_cluster(&tempty[as], aphase ^ 1);
+        const uint64_t tw1 = mtrace ? globaltimer() : 0;
+        uint64_t full_wait = 0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+          if (mtrace) {
+            const uint64_t tf = globaltimer();
+            mbar_wait(&full[stage], phase);
+            full_wait += globaltimer() - tf;
+          } else {
+            mbar_wait(&full[stage], phase);
+          }
           tc_fence_after();
           const uint64_t ad = a_desc0 + (uint64_t)((stage * C::A_BYTES) >> 4);
           const uint64_t bd = b_desc0 + (uint64_t)((stage * C::B_BYTES) >> 4);
@@ -500,6 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) umma_commit<CG>(&tfull[as]);
         __syncwarp();
+        if (mtrace && mslot < p.trace_cap)
+          trace_rec(p, mslot++, (5ull << 56) | (full_wait & 0xFFFFFFFFull), tw0, tw1, w.t);
       }
     }
   } else if (warp == 6) {
