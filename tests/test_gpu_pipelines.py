@@ -565,3 +565,70 @@ def test_wave_lockstep_exact(rng, monkeypatch, world_size):
                 assert np.array_equal(h, ag_ref)
             for y in ys:
                 assert np.array_equal(y, rs_ref[r])
+
+
+@pytest.mark.parametrize("world_size", [1, 2, 4])
+def test_fp16_fused_ops_exact_and_layouts(rng, world_size):
+    # the fp16 instantiation of both fused kernels: integer inputs whose sums
+    # stay below 2048 are exact in fp16, layouts bit-exact
+    F16 = torch.float16
+    rows, n, k = 256, 320, 192
+    m = rows * world_size
+    shape = ProblemShape(m=m, n=n, k=k, dtype="float16")
+    with make_world(world_size, heap_bytes=1 << 26) as w:
+        agb, rsb = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+        shards = [ints(rng, -3, 4, (rows, k)) for _ in range(world_size)]
+        amats = [ints(rng, -2, 3, (m, k)) for _ in range(world_size)]
+        b = ints(rng, -2, 3, (k, n))
+        ag_ref = oracle.ag_gemm_reference(shards, b)
+        rs_ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+        assert np.abs(ag_ref).max() < 2048 and max(np.abs(r).max() for r in rs_ref) < 2048
+
+        def d16(x, pe):
+            return torch.from_numpy(np.ascontiguousarray(x)).to(F16).to(pe.torch_device)
+
+        def body(pe):
+            x, a, bb = d16(shards[pe.rank], pe), d16(amats[pe.rank], pe), d16(b, pe)
+            h = ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, world_size), agb)
+            y = gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, world_size), rsb)
+            return h, y
+
+        for r, (h, y) in enumerate(run_np(w, body)):
+            assert np.array_equal(h, ag_ref)
+            assert np.array_equal(y, rs_ref[r])
+            gathered = to_np(w.read_tensor(r, agb.gathered, F16, (m, k)))
+            assert np.array_equal(gathered, oracle.gathered_layout(shards))
+            staging = to_np(w.read_tensor(r, rsb.staging, F16, (world_size, rows, n)))
+            assert np.array_equal(staging, oracle.staging_layout(amats, [b] * world_size, r))
+
+
+def test_fp16_tp_mlp_float_tolerance():
+    # random-normal fp16 TP MLP pair against an fp32 reference (north-star
+    # tolerance: relative Frobenius error <= 1e-2)
+    W, M, H, F = 2, 512, 256, 384
+    g = np.random.default_rng(7)
+    x_full = g.standard_normal((M, H)).astype(np.float32)
+    ub = [(g.standard_normal((H, F // W)) * 0.05).astype(np.float32) for _ in range(W)]
+    db = [(g.standard_normal((F // W, H)) * 0.05).astype(np.float32) for _ in range(W)]
+    ag_shape = ProblemShape(m=M, n=F // W, k=H, dtype="float16")
+    rs_shape = ProblemShape(m=M, n=H, k=F // W, dtype="float16")
+    rows = M // W
+    with make_world(W, heap_bytes=1 << 24) as w:
+        agb, rsb = make_ag_gemm_buffers(w, ag_shape), make_gemm_rs_buffers(w, rs_shape)
+
+        def h16(x, pe):
+            return torch.from_numpy(x).to(torch.float16).to(pe.torch_device)
+
+        def body(pe):
+            h = ag_gemm(pe, h16(x_full[pe.rank * rows:(pe.rank + 1) * rows], pe),
+                        h16(ub[pe.rank], pe), ag_shape, ag_order_switch(pe.rank, W), agb)
+            return gemm_rs(pe, h, h16(db[pe.rank], pe), rs_shape,
+                           rs_inter_order(pe.ctx, 1, W), rsb)
+
+        res = run_np(w, body)
+    xr = torch.from_numpy(x_full).half().float().numpy()
+    y_full = sum((xr @ torch.from_numpy(ub[r]).half().float().numpy()) @
+                 torch.from_numpy(db[r]).half().float().numpy() for r in range(W))
+    for r, y in enumerate(res):
+        ref = y_full[r * rows:(r + 1) * rows]
+        assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-2
