@@ -58,6 +58,7 @@ struct TileParams {
   uint64_t* trace;
   int trace_cap;
   uint64_t l2_hint_a, l2_hint_b;      // TMA L2 cache policies of the operand loads
+  uint64_t l2_hint_store;             // RS: L2 policy of the staging / output stores
   // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
   // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
   // clusters.  A cluster's range is walked backwards, so the partial head of a
@@ -718,8 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (MODE == MODE_AG) {
               tma_store_3d(&maps.c, sb, xcol, row, chunk);
             } else {
-              tma_store_2d(&maps.out[chunk], sb, xcol, row);
-              if (dual) tma_store_3d(&maps.c, sb, xcol, row, 0);
+              tma_store_2d_hint(&maps.out[chunk], sb, xcol, row, p.l2_hint_store);
+              if (dual) tma_store_3d_hint(&maps.c, sb, xcol, row, 0, p.l2_hint_store);
             }
             bulk_commit();
           }
@@ -782,8 +783,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&maps.out[chunk], own_b, xcol, row);  // staging slot `rank` (layout)
-            tma_store_3d(&maps.c, sum_b, xcol, row, 0);        // the reduced output rows
+            // staging slot `rank` (layout) and the reduced output rows
+            tma_store_2d_hint(&maps.out[chunk], own_b, xcol, row, p.l2_hint_store);
+            tma_store_3d_hint(&maps.c, sum_b, xcol, row, 0, p.l2_hint_store);
             bulk_commit();
           }
           buf = (pair ^ 1) * 2;

@@ -210,6 +210,15 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* s
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap* m, const void* src, int x,
+                                                  int y, int z, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], "
+      "[%1], %5;" ::"l"(m),
+      "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z), "l"(hint)
+      : "memory");
+}
+
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
