@@ -40,6 +40,8 @@ pairs = {
            ("ag cublas", lambda: torch.matmul(x, wu))],
     "rs": [("rs ours", lambda: sb.gemm_rs(pe, h0, wd, rss, sr, rsb, reset=False)),
            ("rs cublas", lambda: torch.matmul(h0, wd))],
+    "core4": [("core C4", lambda: sb.gemm(h0, wd)), ("cublas C4", lambda: torch.matmul(h0, wd))],
+    "core3": [("core C3", lambda: sb.gemm(x, wu)), ("cublas C3", lambda: torch.matmul(x, wu))],
 }
 modes = (sys.argv[1] if len(sys.argv) > 1 else "step").split(",")
 for _ in range(10):

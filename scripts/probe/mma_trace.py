@@ -54,3 +54,9 @@ for kern in ("ag_gemm", "gemm_rs"):
     print(f"   item period              : median {statistics.median(per):.2f} us  mean {statistics.mean(per):.2f}")
     print(f"   first item start after CTA0 start: mean {statistics.mean(first):.2f} us max {max(first):.2f}")
     print(f"   CTA end times: min {min(cta_end):.1f} median {statistics.median(cta_end):.1f} max {max(cta_end):.1f} us")
+for kern in ("ag_gemm", "gemm_rs"):
+    ep = [e for e in ev if e["kernel"] == kern and e["op"] == "tile_epilogue"]
+    launch = max(e["launch"] for e in ep)
+    d = [(e["t1_ns"] - e["t0_ns"]) / 1e3 for e in ep if e["launch"] == launch]
+    print(f"== {kern}: epilogue (accumulator ready -> stores issued, warp 2): "
+          f"median {statistics.median(d):.2f} us  mean {statistics.mean(d):.2f}  max {max(d):.2f}")
