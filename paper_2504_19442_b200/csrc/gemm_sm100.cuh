@@ -360,6 +360,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above (barrier init, TMEM allocation, descriptor prefetch)
+  // overlaps the previous grid's tail under programmatic dependent launch;
+  // every global-memory access comes after this point
+  grid_dependency_wait();
+  grid_launch_dependents();
 
   const int cluster_id = blockIdx.x / CG;
   const int num_clusters = gridDim.x / CG;

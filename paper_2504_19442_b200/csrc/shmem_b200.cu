@@ -278,7 +278,7 @@ int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_
 // kernel dispatch
 
 template <int BN, int CG, int MODE, bool FP16>
-int launch_one(const TensorMaps& maps, const TileParams& p, int grid, cudaStream_t s) {
+int launch_one(const TensorMaps& maps, const TileParams& p, int grid, cudaStream_t s, bool pdl) {
   using C = GemmCfg<BN, CG>;
   auto kern = gemm_tp_kernel<BN, CG, MODE, FP16>;
   // smem attribute + carveout are set per device by preload_kernels()
@@ -287,26 +287,29 @@ int launch_one(const TensorMaps& maps, const TileParams& p, int grid, cudaStream
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, p));
   return SH_OK;
 }
 
 template <int MODE, bool FP16>
-int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaStream_t s) {
+int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaStream_t s,
+                bool pdl) {
   if (c.cg == 2) {
-    if (c.bn == 256) return launch_one<256, 2, MODE, FP16>(maps, p, c.grid, s);
-    if (c.bn == 224) return launch_one<224, 2, MODE, FP16>(maps, p, c.grid, s);
-    return launch_one<128, 2, MODE, FP16>(maps, p, c.grid, s);
+    if (c.bn == 256) return launch_one<256, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
+    if (c.bn == 224) return launch_one<224, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
+    return launch_one<128, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
   }
-  if (c.bn == 256) return launch_one<256, 1, MODE, FP16>(maps, p, c.grid, s);
-  return launch_one<128, 1, MODE, FP16>(maps, p, c.grid, s);
+  if (c.bn == 256) return launch_one<256, 1, MODE, FP16>(maps, p, c.grid, s, pdl);
+  return launch_one<128, 1, MODE, FP16>(maps, p, c.grid, s, pdl);
 }
 
 uint64_t l2_policy(const char* env, uint64_t dflt) {
@@ -317,9 +320,13 @@ uint64_t l2_policy(const char* env, uint64_t dflt) {
   return kEvictNormal;
 }
 
+// Programmatic dependent launch of back-to-back GEMMs on one stream (the
+// next grid's prologue overlaps this grid's tail).  Off for ranks that share
+// a GPU: their persistent grids must stay co-resident.  SHB_PDL=0 disables.
 template <int MODE>
 int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParams& pin,
-                cudaStream_t s) {
+                cudaStream_t s, bool shares_gpu = false) {
+  const bool pdl = !shares_gpu && env_int("SHB_PDL", 1) != 0;
   TileParams p = pin;
   p.l2_hint_a = l2_policy("SHB_HINT_A", kEvictNormal);
   p.l2_hint_b = l2_policy("SHB_HINT_B", kEvictNormal);
@@ -334,8 +341,8 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
             MODE, c.bn, c.cg, c.grid, p.rows, p.n, p.k, p.world, p.rank, p.mblk, p.nblk,
             p.num_tiles, p.dp_tiles, p.group_m, (unsigned long long)p.epoch, p.copy_own,
             p.fuse_reduce, (void*)p.err, (void*)p.ws);
-  if (dtype == SH_DTYPE_FP16) return launch_mode<MODE, true>(c, maps, p, s);
-  return launch_mode<MODE, false>(c, maps, p, s);
+  if (dtype == SH_DTYPE_FP16) return launch_mode<MODE, true>(c, maps, p, s, pdl);
+  return launch_mode<MODE, false>(c, maps, p, s, pdl);
 }
 
 // Load every kernel of this library on `dev` now.  With CUDA lazy loading a
@@ -1160,7 +1167,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   }
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
-  if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s))) return rc;
+  if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s, rs->shares_gpu))) return rc;
 
   // ---- publish "finished reading my gather buffer" to every peer, then
   // join the comm stream so the call completes only when a_shard is free.
@@ -1296,7 +1303,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   p.fuse_reduce = fuse ? 1 : 0;
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
-  if ((rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s))) return rc;
+  if ((rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s, rs->shares_gpu))) return rc;
 
   // reduction of my W staging slots in ascending source order: fused into the
   // epilogue of my own chunk's tiles (scheduled last, rs_inter_order), or a
