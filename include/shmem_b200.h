@@ -171,9 +171,10 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
 /* Tile override for tuning: bn in {0 (auto), 128, 224, 256}; cta_group in {0 (auto), 1, 2}
  * (224 needs cta_group 2). */
 int sh_set_tile_config(int bn, int cta_group);
-/* Tile-order override for tuning: stream_k -1 auto (split the last waves when
- * they would leave CTA pairs idle), 0 off, 1 always; group_m 0 auto (L2
- * budget) or the number of m-blocks walked per n-block. */
+/* Tile-order override for tuning: stream_k -2 unset (env SHB_SK, else auto),
+ * -1 auto (split the last waves when they would leave CTA pairs idle), 0 off,
+ * 1 always; group_m -1 unset (env SHB_GROUP_M, else auto), 0 auto (L2 budget)
+ * or the number of m-blocks walked per n-block. */
 int sh_set_schedule_config(int stream_k, int group_m);
 /* Data-parallel tile hand-out: -1 default (env SHB_DYN, else static), 0 static
  * stride schedule, 1 dynamic (global atomic counter, one tile fetched ahead). */

@@ -909,8 +909,8 @@ int sh_trace_read(sh_world* w, int rank, uint64_t* out_host, size_t out_words, i
 }
 
 int sh_set_schedule_config(int stream_k, int group_m) {
-  if (stream_k < -1 || stream_k > 1) return fail(SH_ERR_ARG, "stream_k must be -1, 0 or 1");
-  if (group_m < 0) return fail(SH_ERR_ARG, "group_m must be >= 0");
+  if (stream_k < -2 || stream_k > 1) return fail(SH_ERR_ARG, "stream_k must be -2, -1, 0 or 1");
+  if (group_m < -1) return fail(SH_ERR_ARG, "group_m must be >= -1");
   g_stream_k = stream_k;
   g_group_m = group_m;
   return SH_OK;
