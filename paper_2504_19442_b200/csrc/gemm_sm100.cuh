@@ -65,6 +65,12 @@ struct TileParams {
   // tile is produced first and the cluster finishing its tail (k_end = K)
   // reduces the partials from the fp32 workspace.
   int dp_tiles;
+  // AG at W>1: the clusters whose first tile belongs to a remote chunk (the
+  // last sk_late clusters when the own chunk has fewer tiles than clusters)
+  // start ~one chunk transfer late; they get sk_late_units fewer stream-K
+  // units so that every cluster finishes together.  0: even partition.
+  int sk_late;
+  int sk_late_units;
   // dynamic scheduling of the data-parallel tiles: the leader CTA's producer
   // claims tile ids from a global counter (zeroed before the launch) and
   // broadcasts them through a small smem ring to every role of the pair, so
@@ -139,6 +145,16 @@ struct TileRing {
 struct WorkIter {
   int t, C, KB, dp;
   long long u0, u, U;
+  // weighted stream-K partition: the last L clusters (late starters) own
+  // y = x - d units each, the others x (see TileParams::sk_late)
+  int L;
+  long long x, y;
+  __device__ __forceinline__ long long start(int i) const {
+    if (L == 0) return U * i / C;
+    const int F = C - L;
+    const long long s = i <= F ? (long long)i * x : (long long)F * x + (long long)(i - F) * y;
+    return s < U ? s : U;
+  }
   // dynamic phase
   TileRing* ring;
   int* counter;
@@ -152,8 +168,15 @@ struct WorkIter {
     dp = p.dp_tiles;
     t = cid;
     U = (long long)(p.num_tiles - dp) * KB;
-    u0 = U * cid / C;
-    u = U * (cid + 1) / C;
+    L = (p.sk_late > 0 && p.sk_late < nclusters && U > 0) ? p.sk_late : 0;
+    if (L) {
+      const long long d = p.sk_late_units;
+      x = (U + (long long)L * d + C - 1) / C;
+      y = x - d;
+      if (y < 1) { L = 0; }  // host clamps d; never an empty or negative share
+    }
+    u0 = start(cid);
+    u = start(cid + 1);
     ring = r;
     counter = p.tile_counter;
     role = ring_role;
@@ -223,11 +246,18 @@ struct WorkIter {
     }
     return false;
   }
-  // first cluster whose range [U*i/C, U*(i+1)/C) contains stream-K unit v
+  // first cluster whose range [start(i), start(i+1)) contains stream-K unit v
   __device__ __forceinline__ int owner(long long v) const {
-    int i = (int)(v * C / U);
-    while (i + 1 < C && U * (i + 1) / C <= v) ++i;
-    while (i > 0 && U * i / C > v) --i;
+    int i;
+    if (L == 0) {
+      i = (int)(v * C / U);
+    } else {
+      const int F = C - L;
+      i = v < (long long)F * x ? (int)(v / x) : F + (int)((v - (long long)F * x) / y);
+      if (i > C - 1) i = C - 1;
+    }
+    while (i + 1 < C && start(i + 1) <= v) ++i;
+    while (i > 0 && start(i) > v) --i;
     return i;
   }
 };

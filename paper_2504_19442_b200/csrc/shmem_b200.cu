@@ -141,6 +141,34 @@ int stream_k_split(const Cfg& c, int num_kb) {
   return full > 1 ? (full - 1) * clusters : 0;
 }
 
+// Weighted stream-K partition for the AG GEMM at W>1 (TileParams::sk_late):
+// with the own chunk first in the order, clusters [tiles_first, clusters)
+// open on the next chunk and wait for its push -- about chunk_bytes over
+// NVLink (770 GB/s measured) -- so their stream-K share shrinks by that many
+// k-block units.  SHB_SK_LATE="L,d" forces the partition (tests at W=1).
+void sk_late_partition(const Cfg& c, TileParams& p, int world, size_t chunk_bytes, int sms) {
+  const int clusters = c.grid / c.cg;
+  const int num_kb = (p.k + 63) / 64;
+  const long long U = (long long)(p.num_tiles - p.dp_tiles) * num_kb;
+  long long L = 0, d = 0;
+  if (const char* e = getenv("SHB_SK_LATE")) {
+    if (sscanf(e, "%lld,%lld", &L, &d) != 2) L = d = 0;
+  } else if (world > 1) {
+    const int tiles_first = p.mblk * p.nblk;
+    if (tiles_first < clusters) {
+      L = clusters - tiles_first;
+      // one k-block of a cluster tile at ~1.4 PFLOP/s spread over the SMs
+      const double t_kb = 2.0 * (128.0 * c.cg) * c.bn * 64.0 / (1.4e15 * c.cg / sms);
+      d = (long long)(chunk_bytes / 770e9 / t_kb);
+    }
+  }
+  const long long cap = U / clusters / 2;  // never more than half a share
+  if (d > cap) d = cap;
+  if (L <= 0 || L >= clusters || d <= 0) return;
+  p.sk_late = (int)L;
+  p.sk_late_units = (int)d;
+}
+
 // fp32 partial workspace for the stream-K tail of one stream of launches.
 struct SkWorkspace {
   float* ws = nullptr;
@@ -337,10 +365,11 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   if (env_int("SHB_TRACE", 0))
     fprintf(stderr,
             "[shb] mode=%d bn=%d cg=%d grid=%d rows=%d n=%d k=%d W=%d rank=%d mblk=%d nblk=%d "
-            "tiles=%d dp=%d group_m=%d epoch=%llu copy_own=%d fuse=%d err=%p ws=%p\n",
+            "tiles=%d dp=%d group_m=%d epoch=%llu copy_own=%d fuse=%d err=%p ws=%p "
+            "late=%d/%d\n",
             MODE, c.bn, c.cg, c.grid, p.rows, p.n, p.k, p.world, p.rank, p.mblk, p.nblk,
             p.num_tiles, p.dp_tiles, p.group_m, (unsigned long long)p.epoch, p.copy_own,
-            p.fuse_reduce, (void*)p.err, (void*)p.ws);
+            p.fuse_reduce, (void*)p.err, (void*)p.ws, p.sk_late, p.sk_late_units);
   if (dtype == SH_DTYPE_FP16) return launch_mode<MODE, true>(c, maps, p, s, pdl);
   return launch_mode<MODE, false>(c, maps, p, s, pdl);
 }
@@ -1156,6 +1185,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     p.ws = rs->sk.ws;
     p.ws_flags = rs->sk.flags;
     p.ws_epoch = ++rs->sk.epoch;
+    if (!p.tile_counter) sk_late_partition(cfg, p, W, chunk_bytes, num_sms(dev));
   }
   p.copy_own = own_by_ce ? 0 : 1;
   if (p.copy_own) {

@@ -40,9 +40,10 @@ def test_fused_ops_fuzz(W, rows, n, k, cg, sk, seed):
         g = np.random.default_rng(seed)
         m = rows * W
         shape = ProblemShape(m=m, n=n, k=k, dtype="bfloat16")
-        shards = [g.integers(-2, 3, (rows, k)) for _ in range(W)]
-        amats = [g.integers(-1, 2, (m, k)) for _ in range(W)]
-        b = g.integers(-1, 2, (k, n))
+        # integer values held in float64 (BLAS oracle, exact)
+        shards = [g.integers(-2, 3, (rows, k)).astype(np.float64) for _ in range(W)]
+        amats = [g.integers(-1, 2, (m, k)).astype(np.float64) for _ in range(W)]
+        b = g.integers(-1, 2, (k, n)).astype(np.float64)
         ag_ref = oracle.ag_gemm_reference(shards, b)
         rs_ref = oracle.gemm_rs_reference(amats, [b] * W)
         if np.abs(ag_ref).max() >= 256 or max(np.abs(r).max() for r in rs_ref) >= 256:

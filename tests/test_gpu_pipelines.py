@@ -65,7 +65,9 @@ def perm_schedule(rank, order):
 
 
 def ints(rng, lo, hi, shape):
-    return rng.integers(lo, hi, shape).astype(np.int64)
+    # integer-valued, held in float64: the oracle's matmuls run on BLAS
+    # (numpy's int64 matmul is a scalar loop) and stay exact at these sizes
+    return rng.integers(lo, hi, shape).astype(np.float64)
 
 
 def dev(x, rank_pe):
@@ -632,3 +634,36 @@ def test_fp16_tp_mlp_float_tolerance():
     for r, y in enumerate(res):
         ref = y_full[r * rows:(r + 1) * rows]
         assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < 1e-2
+
+
+@pytest.mark.parametrize("world_size,rows,n,k,late", [
+    (1, 2560, 2048, 4096, "18,20"),   # forced weighted partition, clipped late shares
+    (1, 2560, 2048, 4096, "40,30"),
+    (4, 512, 2048, 1024, None),       # automatic: own chunk has fewer tiles than clusters
+    (8, 256, 1024, 2048, None),
+])
+def test_ag_weighted_stream_k_partition_exact(rng, monkeypatch, world_size, rows, n, k, late):
+    # the stream-K share of the clusters that open on a remote chunk shrinks by
+    # the expected push time; the fixup owners must follow the same partition
+    if late:
+        monkeypatch.setenv("SHB_SK_LATE", late)
+    monkeypatch.setenv("SHB_SK", "1")
+    shape = ProblemShape(m=rows * world_size, n=n, k=k, dtype="bfloat16")
+    with make_world(world_size, heap_bytes=1 << 27, timeout_s=20.0) as w:
+        bufs = make_ag_gemm_buffers(w, shape)
+        # small integers held in float64: the oracle's matmul runs on BLAS
+        # (numpy's int64 matmul is a scalar loop) and stays exact
+        shards = [ints(rng, -1, 2, (rows, k)).astype(np.float64) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (k, n)).astype(np.float64)
+        ref = oracle.ag_gemm_reference(shards, b)
+        if np.abs(ref).max() >= 256:
+            pytest.skip("not exact in bf16 for this draw")
+
+        def body(pe):
+            x, bb = dev(shards[pe.rank], pe), dev(b, pe)
+            return [ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, world_size), bufs,
+                            reset=False) for _ in range(2)]
+
+        for outs in run_np(w, body):
+            for out in outs:
+                assert np.array_equal(out, ref)
