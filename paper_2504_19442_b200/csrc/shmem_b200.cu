@@ -277,6 +277,17 @@ Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
 // ---------------------------------------------------------------------------
 // tensor maps
 
+// L2 sector promotion of the TMA fetches (SHB_L2_PROMO 0 none, 1 64 B,
+// 2 128 B, 3 256 B = default)
+CUtensorMapL2promotion l2_promotion() {
+  switch (env_int("SHB_L2_PROMO", 3)) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_t* dims,
              const uint64_t* strides_bytes, const uint32_t* box,
              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
@@ -294,8 +305,8 @@ int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_
   CUresult r = d.encode(m, dtype == SH_DTYPE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                         rank, const_cast<void*>(ptr), gd, gs, bx, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, l2_promotion(),
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(SH_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) ptr=%p dims=%llu,%llu", (int)r,
                 ptr, (unsigned long long)dims[0], (unsigned long long)dims[1]);
