@@ -39,6 +39,7 @@ struct TileParams {
   int mblk, nblk;  // m-blocks per chunk, n-blocks
   int num_tiles;   // world * mblk * nblk
   int group_m;     // raster group (m-blocks) for L2 reuse
+  int serpentine;  // odd raster groups walk n backwards
   int order[kMaxWorld];  // chunk visit order (reference swizzle.py)
   uint64_t epoch;
   const uint64_t* ready;              // AG: my pad, ready[src] (written by src)
@@ -285,6 +286,9 @@ __device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chu
   const int in = w - group * span;
   mb = first_m + in % gsize;
   nb = in / gsize;
+  // serpentine: odd groups walk the n-blocks backwards, so a group starts on
+  // the B columns its predecessor finished with (still in L2)
+  if (p.serpentine && (group & 1)) nb = p.nblk - 1 - nb;
 }
 
 template <int BN, int CG>

@@ -373,6 +373,7 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   // the launch, and keeping them out of L2 spares the A/B rows the GEMM still
   // reuses (C4: DRAM reads 259 -> 229 MB per launch)
   p.l2_hint_store = l2_policy("SHB_HINT_STORE", kEvictFirst);
+  p.serpentine = env_int("SHB_SERPENTINE", 1);
   if (env_int("SHB_TRACE", 0))
     fprintf(stderr,
             "[shb] mode=%d bn=%d cg=%d grid=%d rows=%d n=%d k=%d W=%d rank=%d mblk=%d nblk=%d "
