@@ -221,7 +221,10 @@ int raster_group(int rows, int k, int mblk, int bm, int clusters) {
   const int resident = (int)(budget / a_blk);
   int square = 1;
   while ((square + 1) * (square + 1) <= clusters) ++square;
-  return std::max(1, std::min(mblk, std::max(resident, square)));
+  const int g = std::max(1, std::min(mblk, std::max(resident, square)));
+  // equal-sized groups (C4: 16 + 16 instead of 17 + 15; DRAM 216 -> 200 MB)
+  const int ngroups = (mblk + g - 1) / g;
+  return (mblk + ngroups - 1) / ngroups;
 }
 
 Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
