@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if constexpr (MODE == MODE_AG) {
-              tma_store_3d(&maps.c, sb, xcol, row, chunk);
+              tma_store_3d_hint(&maps.c, sb, xcol, row, chunk, p.l2_hint_store);
             } else {
               tma_store_2d_hint(&maps.out[chunk], sb, xcol, row, p.l2_hint_store);
               if (dual) tma_store_3d_hint(&maps.c, sb, xcol, row, 0, p.l2_hint_store);

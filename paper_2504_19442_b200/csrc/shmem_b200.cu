@@ -375,7 +375,8 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   // RS staging / output stores are evict-first: nothing re-reads them during
   // the launch, and keeping them out of L2 spares the A/B rows the GEMM still
   // reuses (C4: DRAM reads 259 -> 229 MB per launch)
-  p.l2_hint_store = l2_policy("SHB_HINT_STORE", kEvictFirst);
+  p.l2_hint_store = MODE == MODE_RS ? l2_policy("SHB_HINT_STORE", kEvictFirst)
+                                     : l2_policy("SHB_HINT_STORE_AG", kEvictNormal);
   p.serpentine = env_int("SHB_SERPENTINE", 1);
   if (env_int("SHB_TRACE", 0))
     fprintf(stderr,
