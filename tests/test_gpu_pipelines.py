@@ -619,13 +619,18 @@ def test_fp16_tp_mlp_float_tolerance():
         agb, rsb = make_ag_gemm_buffers(w, ag_shape), make_gemm_rs_buffers(w, rs_shape)
 
         def h16(x, pe):
-            return torch.from_numpy(x).to(torch.float16).to(pe.torch_device)
+            return torch.from_numpy(np.ascontiguousarray(x)).to(torch.float16).to(pe.torch_device)
+
+        # stage every input first: a pageable host->device copy issued after a
+        # rank's collective could wait behind it while a sibling rank's
+        # launch waits behind the copy (World.run docstring)
+        staged = w.run(lambda pe: (h16(x_full[pe.rank * rows:(pe.rank + 1) * rows], pe),
+                                   h16(ub[pe.rank], pe), h16(db[pe.rank], pe)))
 
         def body(pe):
-            h = ag_gemm(pe, h16(x_full[pe.rank * rows:(pe.rank + 1) * rows], pe),
-                        h16(ub[pe.rank], pe), ag_shape, ag_order_switch(pe.rank, W), agb)
-            return gemm_rs(pe, h, h16(db[pe.rank], pe), rs_shape,
-                           rs_inter_order(pe.ctx, 1, W), rsb)
+            x, up, dn = staged[pe.rank]
+            h = ag_gemm(pe, x, up, ag_shape, ag_order_switch(pe.rank, W), agb)
+            return gemm_rs(pe, h, dn, rs_shape, rs_inter_order(pe.ctx, 1, W), rsb)
 
         res = run_np(w, body)
     xr = torch.from_numpy(x_full).half().float().numpy()
