@@ -40,6 +40,7 @@ struct TileParams {
   int num_tiles;   // world * mblk * nblk
   int group_m;     // raster group (m-blocks) for L2 reuse
   int serpentine;  // odd raster groups walk n backwards
+  int kserp;       // every other data-parallel tile of a cluster walks K backwards
   int order[kMaxWorld];  // chunk visit order (reference swizzle.py)
   uint64_t epoch;
   const uint64_t* ready;              // AG: my pad, ready[src] (written by src)
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       wi.init(p, cluster_id, num_clusters, num_kb, ring, leader ? 0 : 1, CG);
       WorkItem w;
       int waves_issued = 0;  // data-parallel tiles this cluster has issued
+      int dp_seen = 0;       // data-parallel tiles seen (K-direction parity)
       const bool wave_lead = p.wave_flags != nullptr && leader;
       while (wi.next(w)) {
         int chunk, mb, nb;
@@ -440,8 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           landed |= 1u << chunk;
         }
-        int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        // K direction: every other data-parallel tile of this cluster walks K
+        // backwards, so it opens on the k-slices the previous wave touched last
+        const bool rev = p.kserp && w.kind == 0 && dp_item && (dp_seen & 1);
+        if (dp_item) ++dp_seen;
+        for (int i = 0, nk = w.kb1 - w.kb0; i < nk; ++i) {
+          const int kb = rev ? w.kb1 - 1 - i : w.kb0 + i;
           mbar_wait(&empty[stage], phase ^ 1);
           if ((copy_mask >> stage) & 1u) {
             // the own-slot store of the previous occupant must have read it
@@ -455,8 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // full barrier and keeps the stage until its store has read it.
           bool copy_kb = false;
           if (copying) {
-            copy_kb = cr == 0;
-            cr = (cr + 1 == p.nblk) ? 0 : cr + 1;
+            copy_kb = ((kb - nb) % p.nblk + p.nblk) % p.nblk == 0;
             if (copy_kb) copy_mask |= 1u << stage;
           }
           uint8_t* a_dst = sA + stage * C::A_BYTES;
@@ -532,7 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t full_wait = 0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        // stages arrive in the producer's order (either K direction); only
+        // the first MMA of the item starts a fresh accumulator
+        for (int i = 0, nk = w.kb1 - w.kb0; i < nk; ++i) {
           if (mtrace) {
             const uint64_t tf = globaltimer();
             mbar_wait(&full[stage], phase);
@@ -546,8 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
-              umma_f16<CG>(d_tmem, ad + 2 * kk, bd + 128 * kk, IDESC,
-                           (kb != w.kb0) || (kk != 0));
+              umma_f16<CG>(d_tmem, ad + 2 * kk, bd + 128 * kk, IDESC, (i != 0) || (kk != 0));
             umma_commit<CG>(&empty[stage]);
           }
           __syncwarp();
@@ -568,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // gathered[rank] once the MMAs consumed them.  No extra HBM or L2 reads.
     if (MODE == MODE_AG && p.copy_own) {  // whole warp walks the items, lane 0 copies
       uint32_t stage = 0, landed_phase = 0;
+      int dp_seen = 0;
       WorkIter wi;
       wi.init(p, cluster_id, num_clusters, num_kb, ring, 1, CG);
       WorkItem w;
@@ -576,10 +583,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode_tile(p, w.t, chunk, mb, nb);
         const bool copying = chunk == p.rank;
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
-        int cr = copying ? (((w.kb0 - nb) % p.nblk) + p.nblk) % p.nblk : 1;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        const bool dp_item = w.t < p.dp_tiles;
+        const bool rev = p.kserp && w.kind == 0 && dp_item && (dp_seen & 1);
+        if (dp_item) ++dp_seen;
+        for (int i = 0, nk = w.kb1 - w.kb0; i < nk; ++i) {
+          const int kb = rev ? w.kb1 - 1 - i : w.kb0 + i;
           if (copying) {
-            if (cr == 0 && lane == 0) {
+            const bool cr0 = ((kb - nb) % p.nblk + p.nblk) % p.nblk == 0;
+            if (cr0 && lane == 0) {
               // uses of a stage for copies alternate with `stored` acks, so
               // this parity wait is never more than one phase away
               mbar_wait(&alanded_bar[stage], (landed_phase >> stage) & 1u);
@@ -592,8 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               bulk_wait_read<0>();
               mbar_arrive(&stored_bar[stage]);
             }
-            if (cr == 0) landed_phase ^= 1u << stage;
-            cr = (cr + 1 == p.nblk) ? 0 : cr + 1;
+            if (cr0) landed_phase ^= 1u << stage;
           }
           if (++stage == STAGES) stage = 0;
         }

@@ -378,6 +378,9 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   p.l2_hint_store = MODE == MODE_RS ? l2_policy("SHB_HINT_STORE", kEvictFirst)
                                      : l2_policy("SHB_HINT_STORE_AG", kEvictNormal);
   p.serpentine = env_int("SHB_SERPENTINE", 1);
+  // K serpentine: AG C3 DRAM reads 484 -> 427 MB per launch; the RS grid
+  // (C4: K = 3584, 17 tiles per cluster) reads more with it, so AG only
+  p.kserp = env_int("SHB_KSERP", MODE == MODE_AG ? 1 : 0);
   if (env_int("SHB_TRACE", 0))
     fprintf(stderr,
             "[shb] mode=%d bn=%d cg=%d grid=%d rows=%d n=%d k=%d W=%d rank=%d mblk=%d nblk=%d "
