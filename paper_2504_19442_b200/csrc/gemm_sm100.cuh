@@ -61,6 +61,7 @@ struct TileParams {
   int trace_cap;
   uint64_t l2_hint_a, l2_hint_b;      // TMA L2 cache policies of the operand loads
   uint64_t l2_hint_store;             // RS: L2 policy of the staging / output stores
+  uint64_t l2_hint_own;               // AG: L2 policy of the own-slot stores
   // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
   // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
   // clusters.  A cluster's range is walked backwards, so the partial head of a
@@ -446,6 +447,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // backwards, so it opens on the k-slices the previous wave touched last
         const bool rev = p.kserp && w.kind == 0 && dp_item && (dp_seen & 1);
         if (dp_item) ++dp_seen;
+        // (kb - nb) mod nblk, stepped with kb: a division per k-block on the
+        // producer's path between the empty wait and the TMA issue cost 25 %
+        int cr = copying ? ((((rev ? w.kb1 - 1 : w.kb0) - nb) % p.nblk) + p.nblk) % p.nblk : 1;
         for (int i = 0, nk = w.kb1 - w.kb0; i < nk; ++i) {
           const int kb = rev ? w.kb1 - 1 - i : w.kb0 + i;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -461,7 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // full barrier and keeps the stage until its store has read it.
           bool copy_kb = false;
           if (copying) {
-            copy_kb = ((kb - nb) % p.nblk + p.nblk) % p.nblk == 0;
+            copy_kb = cr == 0;
+            if (rev) cr = cr == 0 ? p.nblk - 1 : cr - 1;
+            else cr = cr + 1 == p.nblk ? 0 : cr + 1;
             if (copy_kb) copy_mask |= 1u << stage;
           }
           uint8_t* a_dst = sA + stage * C::A_BYTES;
@@ -586,10 +592,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool dp_item = w.t < p.dp_tiles;
         const bool rev = p.kserp && w.kind == 0 && dp_item && (dp_seen & 1);
         if (dp_item) ++dp_seen;
+        int cr = copying ? ((((rev ? w.kb1 - 1 : w.kb0) - nb) % p.nblk) + p.nblk) % p.nblk : 1;
         for (int i = 0, nk = w.kb1 - w.kb0; i < nk; ++i) {
           const int kb = rev ? w.kb1 - 1 - i : w.kb0 + i;
           if (copying) {
-            const bool cr0 = ((kb - nb) % p.nblk + p.nblk) % p.nblk == 0;
+            const bool cr0 = cr == 0;
+            if (rev) cr = cr == 0 ? p.nblk - 1 : cr - 1;
+            else cr = cr + 1 == p.nblk ? 0 : cr + 1;
             if (cr0 && lane == 0) {
               // uses of a stage for copies alternate with `stored` acks, so
               // this parity wait is never more than one phase away
@@ -598,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // evict-first: 1 B written per 2 B the GEMM keeps reading from
               // L2; don't let the copy push the operands out
               tma_store_2d_hint(&maps.own_slot, sA + stage * C::A_BYTES, kb * BK, row0,
-                                kEvictFirst);
+                                p.l2_hint_own);
               bulk_commit();
               bulk_wait_read<0>();
               mbar_arrive(&stored_bar[stage]);

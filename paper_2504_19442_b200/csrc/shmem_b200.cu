@@ -377,6 +377,7 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   // reuses (C4: DRAM reads 259 -> 229 MB per launch)
   p.l2_hint_store = MODE == MODE_RS ? l2_policy("SHB_HINT_STORE", kEvictFirst)
                                      : l2_policy("SHB_HINT_STORE_AG", kEvictNormal);
+  p.l2_hint_own = l2_policy("SHB_HINT_OWN", kEvictFirst);
   p.serpentine = env_int("SHB_SERPENTINE", 1);
   // K serpentine: AG C3 DRAM reads 484 -> 427 MB per launch; the RS grid
   // (C4: K = 3584, 17 tiles per cluster) reads more with it, so AG only
