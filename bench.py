@@ -461,7 +461,8 @@ def main():
     if not args.no_sweep:
         # short calls (a few ms each): the burst peak is the roofline denominator
         try:
-            sweep = run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, burst)
+            sweep = run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, burst,
+                              sustained)
             world.check_errors(rank)
         except Exception as e:  # noqa: BLE001 -- the sweep must never cost the headline line
             sweep = {"error": f"{type(e).__name__}: {e}"[:300]}
@@ -537,7 +538,7 @@ def sweep_heap_bytes(tp):
                for op, _, s in sweep_shapes(tp))
 
 
-def run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, peak):
+def run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, peak, peak_sustained=None):
     """Both fused ops against the unfused cuBLAS (+ NCCL at N>1) sequence at
     TP=N for every M of C5; per point TFLOPS/GPU and the fraction of the
     BASELINE roofline max(GEMM at the tensor peak, shard bytes over NVLink)."""
@@ -609,7 +610,10 @@ def run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, peak):
                     "ours_tflops_per_gpu": fl / (ms_ours * 1e-3) / 1e12,
                     "unfused_tflops_per_gpu": fl / (ms_unf * 1e-3) / 1e12,
                     "bound": "tensor" if t_gemm >= t_nvl else "nvlink",
-                    "roofline_frac": roof / ms_ours, "unfused_roofline_frac": roof / ms_unf})
+                    "roofline_frac": roof / ms_ours, "unfused_roofline_frac": roof / ms_unf,
+                    "roofline_frac_sustained_peak": (
+                        max(fl / (peak_sustained * 1e12) * 1e3, t_nvl) / ms_ours
+                        if peak_sustained else None)})
         del bufs
     return out
 
