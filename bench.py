@@ -406,30 +406,40 @@ def main():
     y_host = torch.empty((rows, RS["n"]), dtype=torch.bfloat16).pin_memory()
     x_dev = [torch.empty_like(x) for _ in range(2)]
     h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    done_h2d = [torch.cuda.Event() for _ in range(2)]
-    done_use = [torch.cuda.Event() for _ in range(2)]
-    for i in range(k_e2e):
-        slot = i % 2
-        h2d.wait_event(e0)
-        if i >= 2:
-            h2d.wait_event(done_use[slot])
-        with torch.cuda.stream(h2d):
-            x_dev[slot].copy_(x_host, non_blocking=True)
-        done_h2d[slot].record(h2d)
-        stream.wait_event(done_h2d[slot])
-        with torch.cuda.stream(stream):
-            yd = step(x_dev[slot])
-        done_use[slot].record(stream)
-        d2h.wait_stream(stream)
-        with torch.cuda.stream(d2h):
-            y_host.copy_(yd, non_blocking=True)
-            yd.record_stream(d2h)
-    stream.wait_stream(d2h)
-    e1.record(stream)
-    barrier()
+    def e2e_loop(k):
+        """k steps of the host->device->host pipeline; returns (e0, e1)."""
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        done_h2d = [torch.cuda.Event() for _ in range(2)]
+        done_use = [torch.cuda.Event() for _ in range(2)]
+        for i in range(k):
+            slot = i % 2
+            h2d.wait_event(e0)
+            if i >= 2:
+                h2d.wait_event(done_use[slot])
+            with torch.cuda.stream(h2d):
+                x_dev[slot].copy_(x_host, non_blocking=True)
+            done_h2d[slot].record(h2d)
+            stream.wait_event(done_h2d[slot])
+            with torch.cuda.stream(stream):
+                yd = step(x_dev[slot])
+            done_use[slot].record(stream)
+            d2h.wait_stream(stream)
+            with torch.cuda.stream(d2h):
+                y_host.copy_(yd, non_blocking=True)
+                yd.record_stream(d2h)
+        stream.wait_stream(d2h)
+        e1.record(stream)
+        barrier()
+        return e0, e1
+
+    # untimed warm-up of the same pipeline: outputs held by the D2H stream
+    # (record_stream) make the caching allocator grow its pool during the
+    # first steps, and a cudaMalloc inside the timed loop stalls it (measured:
+    # 9.4 ms/step on a first loop, 2.9 ms/step after)
+    e2e_loop(6)
+    e0, e1 = e2e_loop(k_e2e)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / k_e2e)
     # the PCIe floor of that loop: the same H2D of X and D2H of Y, both
     # directions at once on the same pinned buffers, no compute
