@@ -110,6 +110,8 @@ _lib = None
 def load(path: str | None = None):
     """Load (once) and return the C-ABI library; raises if it is missing."""
     global _lib
+    if _lib is not None and path is None:  # hot path of every call: no lock
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib

@@ -125,9 +125,12 @@ class Pe:
 
     @property
     def torch_device(self):
-        import torch
+        dev = self.__dict__.get("_tdev")
+        if dev is None:
+            import torch
 
-        return torch.device("cuda", self.device)
+            dev = self._tdev = torch.device("cuda", self.device)
+        return dev
 
     def stream(self):
         """This rank's CUDA stream (one per rank, so ranks sharing a GPU run

@@ -40,6 +40,7 @@ _DTYPES = {
     "bfloat16": "bfloat16", "bf16": "bfloat16",
     "float16": "float16", "fp16": "float16", "half": "float16",
 }
+_DTYPE_CACHE = {}  # ProblemShape.dtype -> (torch dtype, SH_DTYPE code); host-path cost per call
 
 
 @dataclass(frozen=True)
@@ -63,6 +64,9 @@ class ProblemShape:
 
     @property
     def torch_dtype(self):
+        hit = _DTYPE_CACHE.get(self.dtype)
+        if hit is not None:
+            return hit[0]
         import torch
 
         name = _DTYPES.get(str(self.dtype).replace("torch.", ""))
@@ -70,13 +74,18 @@ class ProblemShape:
             raise ArgumentError(
                 f"dtype {self.dtype!r}: the tensor-core path computes in bf16/fp16 "
                 "(fp32 accumulate); use dtype='bfloat16' or 'float16'")
-        return getattr(torch, name)
+        tdt = getattr(torch, name)
+        code = _lib.SH_DTYPE_FP16 if tdt == torch.float16 else _lib.SH_DTYPE_BF16
+        _DTYPE_CACHE[self.dtype] = (tdt, code)
+        return tdt
 
     @property
     def dtype_code(self):
-        import torch
-
-        return _lib.SH_DTYPE_FP16 if self.torch_dtype == torch.float16 else _lib.SH_DTYPE_BF16
+        hit = _DTYPE_CACHE.get(self.dtype)
+        if hit is None:
+            self.torch_dtype  # noqa: B018 -- validates and fills the cache
+            hit = _DTYPE_CACHE[self.dtype]
+        return hit[1]
 
     @property
     def dtype_bytes(self):
@@ -159,17 +168,20 @@ def _as_device_tensor(x, name, shape, dtype, pe):
     if tuple(x.shape) != tuple(shape) or x.dtype != dtype:
         raise ArgumentError(f"{name} must be {tuple(shape)} of {dtype}, got "
                             f"{tuple(x.shape)} of {x.dtype}")
-    dev = pe.torch_device
-    if x.device.type == "cpu":
-        x = x.to(dev, non_blocking=True)
-    elif x.device != dev:
-        raise ArgumentError(f"{name} lives on {x.device}, rank {pe.rank} runs on {dev}")
-    return x.contiguous()
+    if not x.is_cuda:
+        x = x.to(pe.torch_device, non_blocking=True)
+    elif x.get_device() != pe.device:
+        raise ArgumentError(f"{name} lives on {x.device}, rank {pe.rank} runs on "
+                            f"{pe.torch_device}")
+    return x if x.is_contiguous() else x.contiguous()
 
 
 def _stream_handle(pe):
     import torch
 
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:  # no Stream object per call (host cost of small launches)
+        return raw(pe.device)
     return torch.cuda.current_stream(pe.device).cuda_stream
 
 
