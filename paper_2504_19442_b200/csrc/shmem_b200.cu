@@ -291,9 +291,45 @@ CUtensorMapL2promotion l2_promotion() {
   }
 }
 
+// Per-thread cache of encoded tensor maps: a call's maps are identical to the
+// previous call's whenever the tensors are (the caching allocator hands the
+// same outputs back), and each encode is host time on every launch.
+struct MapKey {
+  const void* ptr;
+  uint64_t dims[3], strides[2];
+  uint32_t box[3];
+  int rank, dtype, swz, promo;
+  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+constexpr int kMapCache = 32;
+struct MapCache {
+  MapKey key[kMapCache];
+  CUtensorMap map[kMapCache];
+  int used = 0, next = 0;
+};
+
 int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_t* dims,
              const uint64_t* strides_bytes, const uint32_t* box,
              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  static thread_local MapCache cache;
+  static const CUtensorMapL2promotion promo = l2_promotion();
+  MapKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.ptr = ptr;
+  for (int i = 0; i < rank; ++i) {
+    key.dims[i] = dims[i];
+    key.box[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) key.strides[i] = strides_bytes[i];
+  key.rank = rank;
+  key.dtype = dtype;
+  key.swz = (int)swz;
+  key.promo = (int)promo;
+  for (int i = 0; i < cache.used; ++i)
+    if (cache.key[i] == key) {
+      *m = cache.map[i];
+      return SH_OK;
+    }
   Driver& d = driver();
   if (!d.ok) return fail(SH_ERR_CUDA, "%s", d.why.c_str());
   cuuint64_t gd[3];
@@ -308,11 +344,14 @@ int make_map(CUtensorMap* m, int dtype, const void* ptr, int rank, const uint64_
   CUresult r = d.encode(m, dtype == SH_DTYPE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                         rank, const_cast<void*>(ptr), gd, gs, bx, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, l2_promotion(),
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(SH_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) ptr=%p dims=%llu,%llu", (int)r,
                 ptr, (unsigned long long)dims[0], (unsigned long long)dims[1]);
+  const int slot = cache.used < kMapCache ? cache.used++ : (cache.next++ % kMapCache);
+  cache.key[slot] = key;
+  cache.map[slot] = *m;
   return SH_OK;
 }
 
