@@ -672,3 +672,37 @@ def test_ag_weighted_stream_k_partition_exact(rng, monkeypatch, world_size, rows
         for outs in run_np(w, body):
             for out in outs:
                 assert np.array_equal(out, ref)
+
+
+def test_tensor_map_cache_same_addresses_new_shapes(rng):
+    # the C ABI caches encoded tensor maps keyed on pointer + layout: calls
+    # that reuse one allocation with other dims / strides must not pick up a
+    # stale map (shmem_b200.cu make_map)
+    shapes = [ProblemShape(m=256, n=192, k=320, dtype="bfloat16"),
+              ProblemShape(m=256, n=128, k=192, dtype="bfloat16"),
+              ProblemShape(m=384, n=256, k=128, dtype="bfloat16")]
+    with make_world(1, heap_bytes=1 << 25) as w:
+        agb = [make_ag_gemm_buffers(w, s) for s in shapes]
+        rsb = [make_gemm_rs_buffers(w, s) for s in shapes]
+        cases = [(i, ints(rng, -2, 3, (s.m, s.k)), ints(rng, -1, 2, (s.k, s.n)))
+                 for _ in range(3) for i, s in enumerate(shapes)]
+
+        def body(pe):
+            pool_a = torch.empty(1 << 20, dtype=BF16, device=pe.torch_device)
+            pool_b = torch.empty(1 << 20, dtype=BF16, device=pe.torch_device)
+            outs = []
+            for i, a, b in cases:
+                s = shapes[i]
+                av = pool_a[: s.m * s.k].view(s.m, s.k)
+                bv = pool_b[: s.k * s.n].view(s.k, s.n)
+                av.copy_(dev(a, pe))
+                bv.copy_(dev(b, pe))
+                outs.append(ag_gemm(pe, av, bv, s, ag_order_switch(0, 1), agb[i]).clone())
+                outs.append(gemm_rs(pe, av, bv, s, rs_inter_order(pe.ctx, 1, 1), rsb[i]).clone())
+            return outs
+
+        outs = run_np(w, body)[0]
+        for j, (i, a, b) in enumerate(cases):
+            assert np.abs(a @ b).max() < 256  # exact in bf16
+            assert np.array_equal(outs[2 * j], a @ b), (j, shapes[i])
+            assert np.array_equal(outs[2 * j + 1], a @ b), (j, shapes[i])
