@@ -1,3 +1,6 @@
+# NOTE: SHB_WAVE=2 (k-granular lockstep) was measured with this script and then
+# removed from the kernel (profiles/README.md, r1_wave_kgran_ab.log); it needs
+# the sources of that experiment to run again.
 # k-granular wave lockstep (SHB_WAVE=2): exactness, DRAM per launch, steady
 # state vs the default and vs the HEAD library (code-layout check)
 nvidia-smi --query-gpu=pci.bus_id,serial --format=csv,noheader
