@@ -15,6 +15,8 @@
  *     bytes; matrices are row-major, dtype bf16 (SH_DTYPE_BF16) or fp16.
  *   - `stream` is a cudaStream_t (may be NULL = legacy default stream); all
  *     device work is enqueued on it (stream-ordered, asynchronous).
+ *     sh_gemm / sh_ag_gemm / sh_gemm_rs refuse a stream under CUDA graph
+ *     capture (SH_ERR_STATE): their epochs are baked into each launch.
  *   - signals are u64 words in a pad at the tail of each rank's slab; a
  *     signal index `sig` addresses slab + heap_bytes + 8*sig on every rank
  *     (reference core.py:242-261).

@@ -707,6 +707,19 @@ int store_flags(cudaStream_t s, uint64_t* const* ptrs, int count, uint64_t value
   return SH_OK;
 }
 
+// Each call bakes its epoch (and the stream-K workspace epoch) into the
+// launch parameters; a captured CUDA graph would replay them with the same
+// epochs and race on its flags, so capture is refused, not silently recorded.
+int refuse_capture(void* stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &st));
+  if (st != cudaStreamCaptureStatusNone)
+    return fail(SH_ERR_STATE,
+                "CUDA graph capture is not supported: epochs are host values baked into "
+                "each launch, a replay would reuse them");
+  return SH_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1052,6 +1065,7 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   if (!a || !b || !c) return fail(SH_ERR_ARG, "null tensor");
   if (!aligned16(a) || !aligned16(b) || !aligned16(c))
     return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
+  if ((rc = refuse_capture(stream))) return rc;
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if ((rc = ensure_preloaded(dev))) return rc;
@@ -1134,6 +1148,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   if (!aligned16(a_shard) || !aligned16(b) || !aligned16(c))
     return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
   if (epoch < 1) return fail(SH_ERR_ARG, "epoch must be >= 1");
+  if ((rc = refuse_capture(stream))) return rc;
   const int rows = m / W;
   const uint64_t es = 2;
   const size_t chunk_bytes = (size_t)rows * k * es;
@@ -1289,6 +1304,7 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   if (!aligned16(a) || !aligned16(b) || !aligned16(out))
     return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
   if (epoch < 1) return fail(SH_ERR_ARG, "epoch must be >= 1");
+  if ((rc = refuse_capture(stream))) return rc;
   const int rows = m / W;
   const uint64_t es = 2;
   const size_t slot_bytes = (size_t)rows * n * es;

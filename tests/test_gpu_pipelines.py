@@ -706,3 +706,30 @@ def test_tensor_map_cache_same_addresses_new_shapes(rng):
             assert np.abs(a @ b).max() < 256  # exact in bf16
             assert np.array_equal(outs[2 * j], a @ b), (j, shapes[i])
             assert np.array_equal(outs[2 * j + 1], a @ b), (j, shapes[i])
+
+
+@pytest.mark.filterwarnings("ignore:The CUDA Graph is empty")
+def test_graph_capture_refused_loudly(rng):
+    # epochs are host values baked into each launch, so a CUDA graph replay
+    # would race on stale flags: capture must fail, not record a wrong graph
+    from paper_2504_19442_b200 import UsageError, gemm
+
+    shape = ProblemShape(m=256, n=128, k=128, dtype="bfloat16")
+    with make_world(1) as w:
+        agb, rsb = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+        pe = w.pe(0)
+        a = dev(ints(rng, -2, 3, (256, 128)), pe)
+        b = dev(ints(rng, -1, 2, (128, 128)), pe)
+        calls = [lambda: ag_gemm(pe, a, b, shape, ag_order_switch(0, 1), agb, reset=False),
+                 lambda: gemm_rs(pe, a, b, shape, rs_inter_order(pe.ctx, 1, 1), rsb,
+                                 reset=False),
+                 lambda: gemm(a, b)]
+        torch.cuda.synchronize()
+        for call in calls:
+            g = torch.cuda.CUDAGraph()
+            with pytest.raises(UsageError, match="graph capture"):
+                with torch.cuda.graph(g):
+                    call()
+        # the library still works after the refused captures
+        out = ag_gemm(pe, a, b, shape, ag_order_switch(0, 1), agb)
+        assert np.array_equal(to_np(out), to_np(a) @ to_np(b))
