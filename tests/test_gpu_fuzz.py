@@ -19,7 +19,12 @@ pytestmark = pytest.mark.gpu
 BF16 = torch.bfloat16
 
 
-def cases(n_cases=12, seed=2024):
+def cases(n_cases=None, seed=None):
+    # a longer soak: SHB_FUZZ_CASES=200 SHB_FUZZ_SEED=7 pytest tests/test_gpu_fuzz.py
+    import os
+
+    n_cases = n_cases or int(os.environ.get("SHB_FUZZ_CASES", "12"))
+    seed = seed if seed is not None else int(os.environ.get("SHB_FUZZ_SEED", "2024"))
     g = np.random.default_rng(seed)
     for i in range(n_cases):
         W = int(g.choice([1, 2, 3, 4, 8]))
