@@ -411,6 +411,10 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   TileParams p = pin;
   p.l2_hint_a = l2_policy("SHB_HINT_A", kEvictNormal);
   p.l2_hint_b = l2_policy("SHB_HINT_B", kEvictNormal);
+  if (MODE == MODE_RS) {  // per-op overrides for the RS operands
+    p.l2_hint_a = l2_policy("SHB_HINT_A_RS", p.l2_hint_a);
+    p.l2_hint_b = l2_policy("SHB_HINT_B_RS", p.l2_hint_b);
+  }
   // RS staging / output stores are evict-first: nothing re-reads them during
   // the launch, and keeping them out of L2 spares the A/B rows the GEMM still
   // reuses (C4: DRAM reads 259 -> 229 MB per launch)
