@@ -105,15 +105,19 @@ SIGNATURES = {
 
 _lock = threading.Lock()
 _lib = None
+_lib_path = None
 
 
 def load(path: str | None = None):
-    """Load (once) and return the C-ABI library; raises if it is missing."""
-    global _lib
+    """Load (once) and return the C-ABI library; raises if it is missing, or
+    if ``path`` names another library than the one already loaded."""
+    global _lib, _lib_path
     if _lib is not None and path is None:  # hot path of every call: no lock
         return _lib
     with _lock:
         if _lib is not None:
+            if path is not None and os.path.realpath(path) != _lib_path:
+                raise ShmemError(f"native library already loaded from {_lib_path}, not {path}")
             return _lib
         p = path or os.environ.get("SHB_LIB") or LIB_PATH
         if not os.path.exists(p):
@@ -125,6 +129,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        _lib_path = os.path.realpath(p)
         _lib = lib
         return lib
 

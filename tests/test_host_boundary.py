@@ -32,6 +32,16 @@ def test_library_loads_and_exports_every_symbol():
     assert lib.sh_ipc_handle_size() == 64
 
 
+def test_load_rejects_a_second_library(tmp_path):
+    lib = _lib.load()
+    assert _lib.load(_lib.LIB_PATH if not os.environ.get("SHB_LIB") else
+                     os.environ["SHB_LIB"]) is lib
+    other = tmp_path / "libother.so"
+    other.write_bytes(b"")
+    with pytest.raises(ShmemError, match="already loaded"):
+        _lib.load(str(other))
+
+
 def test_argument_errors_without_gpu():
     lib = _lib.load()
     # argument validation precedes any CUDA work
