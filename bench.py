@@ -272,9 +272,15 @@ def main():
     w_dn = (torch.randn(RS["k"], RS["n"], device=dev, generator=g) * 0.02).to(torch.bfloat16)
     stream = pe.stream()
 
-    def step(xin):
-        h = sb.ag_gemm(pe, xin, w_up, ag_shape, ag_sched, agb, reset=False)
-        return sb.gemm_rs(pe, h, w_dn, rs_shape, rs_sched, rsb, reset=False)
+    # outputs written into preallocated buffers (out=): a step allocates
+    # nothing, so the caching allocator never grows inside a timed loop
+    h_buf = torch.empty((AG["m"], AG["n"]), dtype=torch.bfloat16, device=dev)
+    y_ring = [torch.empty((rows, RS["n"]), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+
+    def step(xin, y_out=None):
+        h = sb.ag_gemm(pe, xin, w_up, ag_shape, ag_sched, agb, reset=False, out=h_buf)
+        return sb.gemm_rs(pe, h, w_dn, rs_shape, rs_sched, rsb, reset=False,
+                          out=y_ring[0] if y_out is None else y_out)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -319,7 +325,8 @@ def main():
             barrier()
             return max_over_ranks(e0.elapsed_time(e1) / k2)
 
-        ag_ms = loop_ms(lambda: sb.ag_gemm(pe, x, w_up, ag_shape, ag_sched, agb, reset=False))
+        ag_ms = loop_ms(lambda: sb.ag_gemm(pe, x, w_up, ag_shape, ag_sched, agb, reset=False,
+                                           out=h_buf))
         rs_ms = loop_ms(lambda: sb.gemm_rs(pe, h_fixed, w_dn, rs_shape, rs_sched, rsb,
                                            reset=False))
     clk = clocks.summary(t_wall0, t_wall1)
@@ -413,6 +420,7 @@ def main():
         e0.record(stream)
         done_h2d = [torch.cuda.Event() for _ in range(2)]
         done_use = [torch.cuda.Event() for _ in range(2)]
+        done_d2h = [torch.cuda.Event() for _ in range(2)]
         for i in range(k):
             slot = i % 2
             h2d.wait_event(e0)
@@ -422,23 +430,24 @@ def main():
                 x_dev[slot].copy_(x_host, non_blocking=True)
             done_h2d[slot].record(h2d)
             stream.wait_event(done_h2d[slot])
+            if i >= 2:
+                stream.wait_event(done_d2h[slot])  # y_ring[slot] read back
             with torch.cuda.stream(stream):
-                yd = step(x_dev[slot])
+                yd = step(x_dev[slot], y_ring[slot])
             done_use[slot].record(stream)
             d2h.wait_stream(stream)
             with torch.cuda.stream(d2h):
                 y_host.copy_(yd, non_blocking=True)
-                yd.record_stream(d2h)
+            done_d2h[slot].record(d2h)
         stream.wait_stream(d2h)
         e1.record(stream)
         barrier()
         return e0, e1
 
-    # untimed warm-up of the same pipeline: outputs held by the D2H stream
-    # (record_stream) make the caching allocator grow its pool during the
-    # first steps, and a cudaMalloc inside the timed loop stalls it (measured:
-    # 9.4 ms/step on a first loop, 2.9 ms/step after)
-    e2e_loop(6)
+    # untimed warm-up of the same pipeline (pinned buffers, copy engines);
+    # the loop itself allocates nothing: outputs go to a two-slot ring
+    # (out=), each slot reused only after its D2H finished
+    e2e_loop(3)
     e0, e1 = e2e_loop(k_e2e)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / k_e2e)
     # the PCIe floor of that loop: the same H2D of X and D2H of Y, both
@@ -509,7 +518,8 @@ def main():
         "e2e": {"value": STEP_FLOPS * N / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                 "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": rows * RS["n"] * 2,
                 "ms_per_step": e2e_ms,
-                "how": "pinned X H2D + ag_gemm + gemm_rs + Y D2H per step, double-buffered",
+                "how": ("pinned X H2D + ag_gemm + gemm_rs + Y D2H per step, double-buffered, "
+                        "outputs in a preallocated ring (out=)"),
                 "pcie_floor_ms": pcie_ms,
                 "pcie_duplex_gbs": (x.numel() + rows * RS["n"]) * 2 / (pcie_ms * 1e-3) / 1e9,
                 "frac_of_pcie_floor": pcie_ms / e2e_ms},

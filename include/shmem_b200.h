@@ -80,6 +80,11 @@ int sh_signal_ptr(sh_world* w, int rank, int peer, int sig, void** ptr);
 int sh_read_signals(sh_world* w, int rank, int base, int count, uint64_t* out_host);
 int sh_reset_signals(sh_world* w, int rank, int base, int count, void* stream);
 
+/* Release-store `value` into signals [base, base+count) of `rank`'s own pad
+ * on `stream` (recovery: saturating the words satisfies every pending >= wait
+ * of a world whose peer never signalled; World.recover). */
+int sh_fill_signals(sh_world* w, int rank, int base, int count, uint64_t value, void* stream);
+
 /* Device-side timeouts (bounded spins) land in a host-mapped error word per
  * rank; nonzero => SynchronizationFault (reference sched.py:227-238). */
 int sh_poll_error(sh_world* w, int rank, int* code);
@@ -90,7 +95,8 @@ int sh_clear_error(sh_world* w, int rank);
  * allgather_push_intra(wait_all=False) (collectives.py:83-102).
  *   a_shard : (m/W, k) this rank's rows        b : (k, n)        c : (m, n) out
  *   gathered_off : offset of the symmetric (W*m/W*k) gather buffer
- *   ready_base   : W signals; ready[src] = epoch once src's shard landed here
+ *   ready_base   : W signals; ready[src] counts src's landed row ranges:
+ *                  (epoch-1)*S + j once range j of S landed (S = sh_ag_subchunks)
  *   done_base    : W signals; done[p] = epoch once rank p finished the call
  *   chunk_order  : W ints, a permutation (first-visit order of the TileSchedule)
  *   epoch        : monotone call counter (>= 1), identical on every rank */
@@ -107,6 +113,33 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
 int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
                size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
                int dtype, const int* chunk_order, uint64_t epoch, void* stream);
+
+/* Phased variants.  SH_PHASE_ALL is the fused call above.  A call split into
+ * SH_PHASE_COMM then SH_PHASE_COMPUTE (same epoch) never waits on the device
+ * for work a peer has not issued yet, provided every rank's COMM phase has
+ * completed (stream drained + host barrier) before any COMPUTE phase is
+ * enqueued -- the protocol World uses for ranks that share a process when a
+ * kernel-serialising tool (ncu, compute-sanitizer, CUDA_LAUNCH_BLOCKING) is
+ * attached.
+ *   AG: COMM = the shard pushes and their ready flags (on `stream`);
+ *       COMPUTE = the GEMM (flags already set) and the done flags.
+ *   RS: COMM = the GEMM with every tile scattered into its owner's staging
+ *       slot plus the arrival counters (no fused reduction);
+ *       COMPUTE = the ascending-source reduction and the producer flags.
+ * subchunks (AG): row ranges per pushed shard, each with its own flag value
+ * (0 = library policy, sh_ag_subchunks); must agree on every rank. */
+#define SH_PHASE_ALL 0
+#define SH_PHASE_COMM 1
+#define SH_PHASE_COMPUTE 2
+int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, void* c,
+                  size_t gathered_off, int ready_base, int done_base, int m, int n, int k,
+                  int dtype, const int* chunk_order, uint64_t epoch, int subchunks, int phase,
+                  void* stream);
+int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out,
+                  size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
+                  int dtype, const int* chunk_order, uint64_t epoch, int phase, void* stream);
+/* Default sub-chunk count of an AG shard of (m/world, k) (1 = whole shard). */
+int sh_ag_subchunks(int m, int k, int world, int* subchunks);
 
 /* One-sided primitives, stream-ordered on the rank's stream: the Table-1
  * subset the standalone collectives are composed of (reference

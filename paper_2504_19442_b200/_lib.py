@@ -37,6 +37,9 @@ SH_DTYPE_FP16 = 1
 SH_DTYPE_FP32 = 2
 SH_DTYPE_I32 = 3
 SH_DTYPE_I64 = 4
+SH_PHASE_ALL = 0
+SH_PHASE_COMM = 1
+SH_PHASE_COMPUTE = 2
 SH_SIG_SET = 0
 SH_SIG_ADD = 1
 SH_MAX_WORLD = 16
@@ -67,6 +70,8 @@ SIGNATURES = {
                                      ctypes.POINTER(_vp)]),
     "sh_read_signals": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_u64_p]),
     "sh_reset_signals": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]),
+    "sh_fill_signals": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_uint64, _vp]),
     "sh_poll_error": (ctypes.c_int, [_vp, ctypes.c_int, _c_int_p]),
     "sh_clear_error": (ctypes.c_int, [_vp, ctypes.c_int]),
     "sh_ag_gemm": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_int,
@@ -75,6 +80,15 @@ SIGNATURES = {
     "sh_gemm_rs": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_int, _c_int_p, ctypes.c_uint64, _vp]),
+    "sh_ag_gemm_ex": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, _c_int_p, ctypes.c_uint64,
+                                     ctypes.c_int, ctypes.c_int, _vp]),
+    "sh_gemm_rs_ex": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.c_size_t,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, _c_int_p, ctypes.c_uint64,
+                                     ctypes.c_int, _vp]),
+    "sh_ag_subchunks": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int_p]),
     "sh_putmem": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, _vp,
                                  ctypes.c_size_t, _vp]),
     "sh_getmem": (ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_size_t,

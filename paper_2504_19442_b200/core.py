@@ -22,6 +22,7 @@ Two ways to build a world:
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 from collections import deque
@@ -33,7 +34,9 @@ from .errors import (
     CollectiveFault,
     ConfigurationError,
     RangeError,
+    ShmemError,
     SynchronizationFault,
+    UsageError,
 )
 
 SIG_BYTES = 8
@@ -369,6 +372,55 @@ def _multimem_dtype(dtype):
     return table[key]
 
 
+def _typestr_table():
+    import torch
+
+    return {torch.uint8: "|u1", torch.int8: "|i1", torch.bool: "|b1", torch.int16: "<i2",
+            torch.int32: "<i4", torch.int64: "<i8", torch.float16: "<f2", torch.bfloat16: "<V2",
+            torch.float32: "<f4", torch.float64: "<f8"}
+
+
+_TYPESTR = {}  # torch dtype -> __cuda_array_interface__ typestr (filled on first use)
+
+
+def _typestr(dtype):
+    if not _TYPESTR:
+        _TYPESTR.update(_typestr_table())
+    return _TYPESTR.get(dtype)
+
+
+_TOOL_ENV = ("CUDA_INJECTION64_PATH", "NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_PORT_BASE",
+             "NV_SANITIZER_INJECTION_PORT_BASE")
+_TOOL_LIBS = ("libcuda-injection", "libsanitizer-collection", "libTreeLauncherTargetInjection",
+              "libInterceptorInjectionTarget")
+
+
+def serialising_tool():
+    """True when kernels are serialised by a tool: Nsight Compute and
+    compute-sanitizer attach through LD_PRELOAD + an injection library
+    (their launch variables, or the library mapped into this process);
+    CUDA_LAUNCH_BLOCKING=1 serialises every launch.  SHB_PHASED=0/1
+    overrides the detection."""
+    import os
+
+    forced = os.environ.get("SHB_PHASED")
+    if forced is not None and forced != "":
+        return forced not in ("0", "false", "no")
+    if os.environ.get("CUDA_LAUNCH_BLOCKING", "0") not in ("0", ""):
+        return True
+    if any(os.environ.get(v) for v in _TOOL_ENV):
+        return True
+    pre = os.environ.get("LD_PRELOAD", "")
+    if any(lib in pre for lib in _TOOL_LIBS + ("TreeLauncher",)):
+        return True
+    try:
+        with open("/proc/self/maps") as f:
+            maps = f.read()
+    except OSError:
+        return False
+    return any(lib in maps for lib in _TOOL_LIBS)
+
+
 class _HostBarrier:
     def __init__(self, parties):
         self.parties = parties
@@ -454,8 +506,17 @@ class World:
         self.pes = [Pe(self, ctx, self.devices[ctx.rank]) if ctx.rank in self.local_ranks else None
                     for ctx in self.ranks]
         self._barrier_obj = _HostBarrier(len(self.local_ranks))
+        self._phase_obj = _HostBarrier(len(self.local_ranks))
+        self._host_obj = _HostBarrier(len(self.local_ranks))
+        self._host_obj = _HostBarrier(len(self.local_ranks))
         self._workers = None
         self._dist = _member is not None
+        self._broken = None   # reason a rank's device work never drained (see recover)
+        self._seq = 0         # run() job sequence (stale results of a timed-out job are dropped)
+        # Ranks of this process that wait on each other's kernels assume those
+        # kernels run concurrently.  Under a kernel-serialising tool they do
+        # not, so the fused ops split into phases joined on the host.
+        self.phased = len(self.local_ranks) > 1 and serialising_tool()
 
     # ------------------------------------------------------------------
     # geometry
@@ -523,11 +584,13 @@ class World:
 
         import torch
 
+        typestr = _typestr(dtype)
+        if typestr is None:
+            raise ArgumentError(f"heap views support {sorted(str(t) for t in _TYPESTR)}, "
+                                f"not {dtype}")
         nbytes = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
         handle.check(off, nbytes)
         ptr = self.heap_ptr(rank, handle, off, peer=peer)
-        typestr = {torch.uint8: "|u1", torch.bfloat16: "<V2", torch.float16: "<f2",
-                   torch.int64: "<i8", torch.float32: "<f4"}[dtype]
 
         class _Arr:
             __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
@@ -595,14 +658,35 @@ class World:
                                               ctypes.c_void_p(stream or 0)))
 
     def zero_all_signals(self):
+        with self._quiescent():
+            for r in self.local_ranks:
+                self.zero_signals(r, 0, self.spec.signal_count)
+        for holder in self._epoch_holders:
+            holder.reset_epochs()
+
+    @contextlib.contextmanager
+    def _quiescent(self):
+        """Zeroing window for signal words.  Peers write this rank's flags
+        from their own streams (done / producer releases after their GEMMs),
+        so every local device is drained and -- one process per GPU -- every
+        process has drained (barrier) before the words are cleared, and no
+        process starts a new call, whose first act is writing peers' flags,
+        before every process has cleared its own (second barrier)."""
         import torch
 
         for r in self.local_ranks:
             torch.cuda.synchronize(self._dev_of(r))
-            self.zero_signals(r, 0, self.spec.signal_count)
+        if self._dist:
+            import torch.distributed as dist
+
+            dist.barrier()
+        yield
+        for r in self.local_ranks:
             torch.cuda.synchronize(self._dev_of(r))
-        for holder in self._epoch_holders:
-            holder.reset_epochs()
+        if self._dist:
+            import torch.distributed as dist
+
+            dist.barrier()
 
     def sweep_signals(self):
         """{(rank, sig): value} for every nonzero signal word of local ranks."""
@@ -661,13 +745,53 @@ class World:
                 f"rank {rank}: device wait on {what} exceeded {self.spec.timeout_s} s")
 
     def recover(self):
-        """Clear device error words and host rendezvous state (core.py:489-493)."""
+        """Clear device error words and host rendezvous state (core.py:489-493).
+
+        A world left broken by a stream that never drained (a stream-side
+        wait on a flag nobody released -- a peer that died) is first
+        unblocked: every local signal word is saturated from a side stream,
+        which satisfies any pending >= wait.  Every wait on the way is
+        bounded; if a stream still does not drain the world stays broken and
+        ShmemError says so (only a new process clears a wedged GPU queue)."""
+        import time
+
         import torch
 
+        if self._broken:
+            deadline = time.monotonic() + 10.0
+            for r in self.local_ranks:
+                dev = self._dev_of(r)
+                with torch.cuda.device(dev):
+                    side = torch.cuda.Stream(device=dev)
+                    # the library's own preloaded kernel: a first launch of a
+                    # lazily loaded (torch) kernel would synchronise the
+                    # context against the blocked stream
+                    _lib.check(self._lib.sh_fill_signals(self._handle, r, 0,
+                                                         self.spec.signal_count, 1 << 62,
+                                                         ctypes.c_void_p(side.cuda_stream)))
+                    while not side.query() and time.monotonic() < deadline:
+                        time.sleep(1e-3)
+            for r in self.local_ranks:
+                pe = self.pes[r]
+                if pe is not None and pe._stream is not None:
+                    while not pe._stream.query() and time.monotonic() < deadline:
+                        time.sleep(1e-3)
+                    if not pe._stream.query():
+                        raise ShmemError(f"{self._broken}; the stream is still blocked after "
+                                         "releasing every signal -- restart the process")
         for r in self.local_ranks:
             torch.cuda.synchronize(self._dev_of(r))
             _lib.check(self._lib.sh_clear_error(self._handle, r))
+        if self._broken:
+            for r in self.local_ranks:
+                self.zero_signals(r, 0, self.spec.signal_count)
+                torch.cuda.synchronize(self._dev_of(r))
+            for holder in self._epoch_holders:
+                holder.reset_epochs()
+            self._broken = None
         self._barrier_obj = _HostBarrier(len(self.local_ranks))
+        self._phase_obj = _HostBarrier(len(self.local_ranks))
+        self._host_obj = _HostBarrier(len(self.local_ranks))
 
     # ------------------------------------------------------------------
     # epochs / reset
@@ -683,18 +807,19 @@ class World:
     def _apply_resets(self):
         """After a join every rank is past every flag of the finished calls,
         so zeroing is race-free (the epoch protocol needs no reset in between;
-        this restores the reference's flag hygiene, collectives.py:67-69)."""
-        import torch
+        this restores the reference's flag hygiene, collectives.py:67-69).
+        With one process per GPU the join is the barrier pair of
+        ``_quiescent``: a call is rank-collective, so every process requests
+        the same resets and reaches this point (reference collectives.py:1-10)."""
 
         with self._reset_lock:
             sets, self._reset_sets = self._reset_sets, set()
         if not sets:
             return
-        for r in self.local_ranks:
-            torch.cuda.synchronize(self._dev_of(r))
-            for s in sets:
-                self.zero_signals(r, s.base, s.count)
-            torch.cuda.synchronize(self._dev_of(r))
+        with self._quiescent():
+            for r in self.local_ranks:
+                for s in sets:
+                    self.zero_signals(r, s.base, s.count)
         for holder in self._epoch_holders:
             holder.reset_epochs_for(sets)
 
@@ -712,6 +837,39 @@ class World:
         else:
             self._barrier_obj.wait(self.spec.timeout_s * 4 + 30)
 
+    def _phase_join(self, pe):
+        """Host join between the phases of a phased fused call: this rank's
+        stream has drained (its pushes / scatters have landed) and so have
+        every other local rank's."""
+        import torch
+
+        torch.cuda.current_stream(pe.device).synchronize()
+        self._phase_obj.wait(self.spec.timeout_s * 4 + 30)
+
+    def _host_join(self, pe):
+        """Rendezvous of the local rank threads before a collective with host
+        operands is issued (no device synchronisation)."""
+        self._host_obj.wait(self.spec.timeout_s * 4 + 30)
+
+    def _drain(self, pe, stream):
+        """Wait for the rank's stream with a host deadline.  Device spins are
+        bounded and report through the error word; a stream-side wait on a
+        flag nobody writes (a peer that died) is not, so the host gives up
+        after the reference's deadline (core.py:467-468) and the world needs
+        recover()."""
+        import time
+
+        deadline = time.monotonic() + self.spec.timeout_s * 4 + 30
+        nap = 5e-5
+        while not stream.query():
+            self.check_errors(pe.rank)
+            if time.monotonic() > deadline:
+                self._broken = (f"rank {pe.rank}: device work did not drain within "
+                                f"{self.spec.timeout_s * 4 + 30:.0f} s")
+                raise SynchronizationFault(self._broken + " (a flag was never released)")
+            time.sleep(nap)
+            nap = min(nap * 2, 2e-3)
+
     def _run_rank(self, fn, rank):
         import torch
 
@@ -721,7 +879,7 @@ class World:
         s.wait_stream(torch.cuda.current_stream(pe.device))
         with torch.cuda.stream(s):
             val = fn(pe)
-        s.synchronize()
+        self._drain(pe, s)
         self.check_errors(rank)
         return val
 
@@ -737,6 +895,8 @@ class World:
         stream is waiting for.  Stage inputs first, return device tensors."""
         if self._closed:
             raise ConfigurationError("world is closed")
+        if self._broken:
+            raise UsageError(f"world needs recover(): {self._broken}")
         ranks = self.local_ranks
         if len(ranks) == 1:
             try:
@@ -747,17 +907,33 @@ class World:
             self._apply_resets()
             return res
         self._ensure_workers()
+        self._seq += 1
+        seq = self._seq
         for r in ranks:
-            self._jobs[r].append(fn)
+            self._jobs[r].append((seq, fn))
             self._job_ev[r].set()
         wait_s = (timeout or self.spec.timeout_s) * 4.0 + 60.0
         results, failures = {}, {}
+        import time
+
+        deadline = time.monotonic() + wait_s
         for r in ranks:
-            if not self._done_ev[r].wait(wait_s):
+            got = None
+            while got is None:
+                left = deadline - time.monotonic()
+                if left <= 0 or not self._done_ev[r].wait(left):
+                    break
+                with self._result_lock:
+                    self._done_ev[r].clear()
+                    tagged = self._results.pop(r, None)
+                    # a result of an earlier job that timed out is dropped
+                    if tagged is not None and tagged[0] == seq:
+                        got = tagged[1:]
+            if got is None:
                 failures[r] = TimeoutError(f"rank {r} did not finish")
+                self._broken = f"rank {r} did not finish job {seq}"
                 continue
-            self._done_ev[r].clear()
-            ok, val = self._results[r]
+            ok, val = got
             if ok:
                 results[r] = val
             else:
@@ -777,6 +953,7 @@ class World:
         self._job_ev = {r: threading.Event() for r in self.local_ranks}
         self._done_ev = {r: threading.Event() for r in self.local_ranks}
         self._results = {}
+        self._result_lock = threading.Lock()
         self._workers = []
         for r in self.local_ranks:
             t = threading.Thread(target=self._worker_loop, args=(r,), daemon=True, name=f"rank{r}")
@@ -790,12 +967,14 @@ class World:
             if self._closed:
                 return
             while self._jobs[rank]:
-                fn = self._jobs[rank].popleft()
+                seq, fn = self._jobs[rank].popleft()
                 try:
-                    self._results[rank] = (True, self._run_rank(fn, rank))
+                    res = (seq, True, self._run_rank(fn, rank))
                 except BaseException as exc:  # noqa: BLE001
-                    self._results[rank] = (False, exc)
-                self._done_ev[rank].set()
+                    res = (seq, False, exc)
+                with self._result_lock:
+                    self._results[rank] = res
+                    self._done_ev[rank].set()
 
     def close(self):
         if self._closed:
@@ -808,10 +987,17 @@ class World:
             try:
                 import torch
 
+                if self._broken:
+                    self.recover()
                 for r in self.local_ranks:
                     torch.cuda.synchronize(self._dev_of(r))
             except Exception:  # noqa: BLE001
                 pass
+            if self._broken:
+                # a wedged stream would hang the destroy's device drain: leak
+                # the slabs instead (the process is expected to exit)
+                self._handle = ctypes.c_void_p()
+                return
             self._lib.sh_world_destroy(self._handle)
             self._handle = ctypes.c_void_p()
 

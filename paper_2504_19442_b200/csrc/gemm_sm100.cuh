@@ -44,6 +44,8 @@ struct TileParams {
   int order[kMaxWorld];  // chunk visit order (reference swizzle.py)
   uint64_t epoch;
   const uint64_t* ready;              // AG: my pad, ready[src] (written by src)
+  int ag_sub;                         // AG: row ranges per pushed shard (ready counts them)
+  int ag_sub_rows;                    // AG: rows per range (multiple of 256)
   uint64_t* rs_count[kMaxWorld];      // RS: &pad_d[reduction + rank]
   const uint64_t* rs_free;            // RS: my pad, producer[d] >= epoch-1: d reduced last call
   const uint64_t* rs_mine;            // RS: my pad, reduction[s] (elements delivered by s)
@@ -412,7 +414,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // registers); one elected lane issues the barrier/TMA instructions.
     {
       uint32_t stage = 0, phase = 0;
-      uint32_t landed = 0;  // chunks whose ready flag this CTA has observed
+      // row ranges of each chunk this CTA has observed landed (ready[c] counts
+      // ranges: (epoch-1)*ag_sub + ranges landed so far)
+      int landed[kMaxWorld];
+#pragma unroll
+      for (int c = 0; c < kMaxWorld; ++c) landed[c] = 0;
       int trace_slot = 1;   // slot 0: CTA lifetime (written by the epilogue)
       uint32_t copy_mask = 0, stored_phase = 0;  // stages holding an own-slot copy
       const uint64_t b_hint = p.l2_hint_b, a_hint = p.l2_hint_a;
@@ -432,16 +438,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool copying = own && p.copy_own;
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
         const int col0 = nb * BN + (int)cta_rank * BNC;
-        if (MODE == MODE_AG && !own && !((landed >> chunk) & 1u)) {
-          // wait(ready[chunk]) of pipelines.py:130-141, as an acquire spin
-          if (lane == 0) {
-            const uint64_t tw0 = p.trace ? globaltimer() : 0;
-            spin_geq(p.ready + chunk, p.epoch, p.err, p.timeout_ns, 1);
-            fence_proxy_async_global();
-            if (p.trace) trace_rec(p, trace_slot++, (1ull << 56) | chunk, tw0, globaltimer(), w.t);
+        if (MODE == MODE_AG && !own) {
+          // wait(ready[chunk]) of pipelines.py:130-141, as an acquire spin on
+          // the range holding this CTA's last row of the tile
+          const int need = (min(row0 + BM, p.rows) - 1) / p.ag_sub_rows + 1;
+          if (landed[chunk] < need) {
+            if (lane == 0) {
+              const uint64_t tw0 = p.trace ? globaltimer() : 0;
+              spin_geq(p.ready + chunk, (p.epoch - 1) * (uint64_t)p.ag_sub + need, p.err,
+                       p.timeout_ns, 1);
+              fence_proxy_async_global();
+              if (p.trace)
+                trace_rec(p, trace_slot++, (1ull << 56) | ((uint64_t)need << 32) | chunk, tw0,
+                          globaltimer(), w.t);
+            }
+            __syncwarp();
+            landed[chunk] = need;
           }
-          __syncwarp();
-          landed |= 1u << chunk;
         }
         // K direction: every other data-parallel tile of this cluster walks K
         // backwards, so it opens on the k-slices the previous wave touched last
@@ -1108,6 +1121,13 @@ __global__ void flag_store_list_kernel(const __grid_constant__ FlagList l, int c
     __threadfence_system();
     st_release_sys(l.ptr[i], value);
   }
+}
+
+// Release-store `value` into `count` consecutive signal words (recovery of a
+// world whose stream waits on flags nobody will release).
+__global__ void flag_fill_kernel(uint64_t* words, int count, uint64_t value) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+    st_release_sys(words + i, value);
 }
 
 // Stream-side wait on a local flag (used only when stream memory operations

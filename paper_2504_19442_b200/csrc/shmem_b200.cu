@@ -169,6 +169,19 @@ void sk_late_partition(const Cfg& c, TileParams& p, int world, size_t chunk_byte
   p.sk_late_units = (int)d;
 }
 
+// Sub-chunk count of the AG pushes (see sh_ag_gemm_ex): a late cluster whose
+// first tile sits in the first remote chunk waits for its own row range
+// rather than the whole shard (C3/TP=8: 4 MB, ~5 us at 770 GB/s, instead of
+// 16 MB).  Small shards stay whole (the per-range flag write is a stream
+// memory op, ~2 us of copy-engine issue each).  SHB_AG_SUB=S forces S.
+int ag_subchunks(int rows, int k, int world) {
+  if (world <= 1) return 1;
+  if (const char* e = getenv("SHB_AG_SUB")) return std::max(1, std::min(64, atoi(e)));
+  const double bytes = (double)rows * k * 2;
+  if (bytes < 8.0 * (1 << 20)) return 1;
+  return std::max(1, std::min(4, rows / 256));
+}
+
 // fp32 partial workspace for the stream-K tail of one stream of launches.
 struct SkWorkspace {
   float* ws = nullptr;
@@ -491,7 +504,8 @@ int preload_kernels(int dev) {
                          reinterpret_cast<const void*>(rs_reduce_kernel<true>),
                          reinterpret_cast<const void*>(flag_store_kernel),
                          reinterpret_cast<const void*>(flag_store_list_kernel),
-                         reinterpret_cast<const void*>(flag_wait_kernel)};
+                         reinterpret_cast<const void*>(flag_wait_kernel),
+                         reinterpret_cast<const void*>(flag_fill_kernel)};
   for (const void* f : small) {
     cudaFuncAttributes a;
     CUDA_TRY(cudaFuncGetAttributes(&a, f));
@@ -581,6 +595,11 @@ int check_shape(int m, int n, int k, int world, int dtype) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// The reduction is fused into the own chunk's epilogue unless the call is
+// phased (its tiles would wait on peers whose GEMM a serialising tool may
+// never run concurrently) or SHB_RS_UNFUSED=1 asks for the separate pass.
+bool rs_fused(int phase) { return phase == SH_PHASE_ALL && env_int("SHB_RS_UNFUSED", 0) == 0; }
 
 }  // namespace
 
@@ -952,6 +971,23 @@ int sh_reset_signals(sh_world* w, int rank, int base, int count, void* stream) {
   return SH_OK;
 }
 
+int sh_fill_signals(sh_world* w, int rank, int base, int count, uint64_t value, void* stream) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (base < 0 || count < 0 || base + count > w->signal_count)
+    return fail(SH_ERR_ARG, "signals [%d, %d) outside pad of %d", base, base + count,
+                w->signal_count);
+  if (count == 0) return SH_OK;
+  CUDA_TRY(cudaSetDevice(rs->device));
+  // a kernel of this (preloaded) module: a first launch of a lazily loaded
+  // kernel would synchronise the context -- against the very stream that is
+  // blocked on these words
+  flag_fill_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(sig_addr(w, *rs, rank, base),
+                                                                     count, value);
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
 int sh_poll_error(sh_world* w, int rank, int* code) {
   RankState* rs = rank_of(w, rank);
   if (!rs || !code) return fail(SH_ERR_ARG, "bad rank %d", rank);
@@ -1140,9 +1176,24 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
 // ---------------------------------------------------------------------------
 // fused AllGather + GEMM
 
+int sh_ag_subchunks(int m, int k, int world, int* subchunks) {
+  if (!subchunks) return fail(SH_ERR_ARG, "null argument");
+  if (m < 1 || k < 1 || world < 1 || m % world) return fail(SH_ERR_ARG, "bad shape");
+  *subchunks = ag_subchunks(m / world, k, world);
+  return SH_OK;
+}
+
 int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* c,
                size_t gathered_off, int ready_base, int done_base, int m, int n, int k, int dtype,
                const int* chunk_order, uint64_t epoch, void* stream) {
+  return sh_ag_gemm_ex(w, rank, a_shard, b, c, gathered_off, ready_base, done_base, m, n, k, dtype,
+                       chunk_order, epoch, 0, SH_PHASE_ALL, stream);
+}
+
+int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, void* c,
+                  size_t gathered_off, int ready_base, int done_base, int m, int n, int k,
+                  int dtype, const int* chunk_order, uint64_t epoch, int subchunks, int phase,
+                  void* stream) {
   RankState* rs = rank_of(w, rank);
   if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
   const int W = w->world;
@@ -1152,6 +1203,8 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   if (!aligned16(a_shard) || !aligned16(b) || !aligned16(c))
     return fail(SH_ERR_ARG, "tensors must be 16-byte aligned");
   if (epoch < 1) return fail(SH_ERR_ARG, "epoch must be >= 1");
+  if (phase < SH_PHASE_ALL || phase > SH_PHASE_COMPUTE)
+    return fail(SH_ERR_ARG, "unknown phase %d", phase);
   if ((rc = refuse_capture(stream))) return rc;
   const int rows = m / W;
   const uint64_t es = 2;
@@ -1172,11 +1225,21 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
       seen |= 1u << ch;
     }
   }
+  // Sub-chunk flags: the push of a shard is split into S row ranges of
+  // sub_rows rows (a multiple of 256, so every m-block of either tile height
+  // lies in one range); after range j lands, ready[src] = (epoch-1)*S + j+1.
+  // One monotone word per source, so S=1 is the plain per-chunk flag.
+  if (subchunks < 0 || subchunks > 64) return fail(SH_ERR_ARG, "subchunks %d outside 0..64", subchunks);
+  const int S = W == 1 ? 1 : (subchunks ? subchunks : ag_subchunks(rows, k, W));
+  const int sub_rows = S > 1 ? ((rows + S - 1) / S + 255) / 256 * 256 : rows;
+  const int S_eff = (rows + sub_rows - 1) / sub_rows;  // a rounding may merge ranges
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = rs->device;
   Cfg cfg = choose_cfg(rows, W, n, num_sms(dev), rs->ranks_on_device);
   const bool own_by_ce = env_int("SHB_OWN_COPY_CE", 0) != 0;
+  const bool do_comm = phase != SH_PHASE_COMPUTE;
+  const bool do_compute = phase != SH_PHASE_COMM;
 
   // ---- comm half: push own shard into every rank's slot `rank`
   // (allgather_push_intra, collectives.py:95-97).  Copy engine, in the order
@@ -1187,32 +1250,44 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   // Ranks sharing a GPU push on the caller's stream ahead of the GEMM: a
   // side stream's copies could otherwise be queued behind another rank's
   // spinning GEMM on the same device (measured: 13/30 W=8 runs stalled).
-  const bool push_on_main = rs->shares_gpu || env_int("SHB_PUSH_ON_MAIN", 0) != 0;
+  // A phased call (SH_PHASE_COMM) pushes on the caller's stream too, so
+  // draining that stream means the pushes and their flags have landed.
+  const bool push_on_main =
+      rs->shares_gpu || phase != SH_PHASE_ALL || env_int("SHB_PUSH_ON_MAIN", 0) != 0;
   // nothing to push (TP=1, own slot written by the GEMM): keep the side
   // stream out of it entirely -- cross-stream event pairs measured to
   // serialise the caller's pinned copies on other streams at TP=1
-  const bool use_comm = !push_on_main && (W > 1 || own_by_ce);
+  const bool use_comm = do_comm && !push_on_main && (W > 1 || own_by_ce);
   cudaStream_t cs = use_comm ? rs->comm : s;
   if (use_comm) {
     CUDA_TRY(cudaEventRecord(rs->ev_in, s));
     CUDA_TRY(cudaStreamWaitEvent(rs->comm, rs->ev_in, 0));
   }
   char* own_gathered = static_cast<char*>(rs->peer[rank]) + gathered_off;
-  for (int step = 1; step < W; ++step) {
-    int p = (rank - step + W) % W;
-    if ((rc = stream_wait_geq(*rs, cs, sig_addr(w, *rs, rank, done_base + p), epoch - 1,
-                              w->timeout_ns)))
-      return rc;
-    char* dst = static_cast<char*>(rs->peer[p]) + gathered_off + (size_t)rank * chunk_bytes;
-    CUDA_TRY(cudaMemcpyAsync(dst, a_shard, chunk_bytes, cudaMemcpyDeviceToDevice, cs));
-    uint64_t* f = sig_addr(w, *rs, p, ready_base + rank);
-    if ((rc = store_flags(cs, &f, 1, epoch))) return rc;
+  if (do_comm) {
+    const size_t row_bytes = (size_t)k * es;
+    for (int step = 1; step < W; ++step) {
+      int p = (rank - step + W) % W;
+      if ((rc = stream_wait_geq(*rs, cs, sig_addr(w, *rs, rank, done_base + p), epoch - 1,
+                                w->timeout_ns)))
+        return rc;
+      char* dst = static_cast<char*>(rs->peer[p]) + gathered_off + (size_t)rank * chunk_bytes;
+      uint64_t* f = sig_addr(w, *rs, p, ready_base + rank);
+      for (int j = 0; j < S_eff; ++j) {
+        const size_t r0 = (size_t)j * sub_rows;
+        const size_t nr = std::min<size_t>(sub_rows, rows - r0);
+        CUDA_TRY(cudaMemcpyAsync(dst + r0 * row_bytes, static_cast<const char*>(a_shard) + r0 * row_bytes,
+                                 nr * row_bytes, cudaMemcpyDeviceToDevice, cs));
+        if ((rc = store_flags(cs, &f, 1, (epoch - 1) * (uint64_t)S_eff + j + 1))) return rc;
+      }
+    }
+    // own slot: written by the GEMM's idle epilogue warps from L2-hot rows
+    // (own_dst below); the copy-engine path stays available for A/B checks
+    if (own_by_ce)
+      CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
+                               cudaMemcpyDeviceToDevice, cs));
   }
-  // own slot: written by the GEMM's idle epilogue warps from L2-hot rows
-  // (own_dst below); the copy-engine path stays available for A/B checks
-  if (own_by_ce)
-    CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
-                             cudaMemcpyDeviceToDevice, cs));
+  if (!do_compute) return SH_OK;
 
   // ---- compute half on the caller's stream
   TensorMaps maps;
@@ -1251,6 +1326,8 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
+  p.ag_sub = S_eff;
+  p.ag_sub_rows = sub_rows;
   attach_trace(*rs, p, MODE_AG);
   if (dynamic_tiles()) {
     p.tile_counter = rs->tile_counter;
@@ -1263,7 +1340,9 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
     p.ws = rs->sk.ws;
     p.ws_flags = rs->sk.flags;
     p.ws_epoch = ++rs->sk.epoch;
-    if (!p.tile_counter) sk_late_partition(cfg, p, W, chunk_bytes, num_sms(dev));
+    // with sub-chunk flags the late clusters wait for the first range only
+    if (!p.tile_counter)
+      sk_late_partition(cfg, p, W, chunk_bytes * (S_eff + 1) / (2 * S_eff), num_sms(dev));
   }
   p.copy_own = own_by_ce ? 0 : 1;
   if (p.copy_own) {
@@ -1275,7 +1354,8 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
   }
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
-  if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s, rs->shares_gpu))) return rc;
+  if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s, rs->shares_gpu || phase != SH_PHASE_ALL)))
+    return rc;
 
   // ---- publish "finished reading my gather buffer" to every peer, then
   // join the comm stream so the call completes only when a_shard is free.
@@ -1299,6 +1379,15 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
 int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
                size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
                int dtype, const int* chunk_order, uint64_t epoch, void* stream) {
+  return sh_gemm_rs_ex(w, rank, a, b, out, staging_off, producer_base, reduction_base, m, n, k,
+                       dtype, chunk_order, epoch, SH_PHASE_ALL, stream);
+}
+
+int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out,
+                  size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
+                  int dtype, const int* chunk_order, uint64_t epoch, int rs_phase, void* stream) {
+  if (rs_phase < SH_PHASE_ALL || rs_phase > SH_PHASE_COMPUTE)
+    return fail(SH_ERR_ARG, "unknown phase %d", rs_phase);
   RankState* rs = rank_of(w, rank);
   if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
   const int W = w->world;
@@ -1331,7 +1420,20 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device), rs->ranks_on_device);
-  const bool fuse = env_int("SHB_RS_UNFUSED", 0) == 0;
+  const bool fuse = rs_fused(rs_phase);
+  // With the reduction fused, the tiles of my own chunk wait for every peer's
+  // rows; a cluster that reached them before finishing its peer-chunk tiles
+  // would hold back rows a peer is waiting for, on every rank at once.  The
+  // own chunk therefore always runs last (the result does not depend on the
+  // order: the reduction is ascending by source whatever the schedule).
+  int order[SH_MAX_WORLD];
+  {
+    int j = 0;
+    for (int i = 0; i < W; ++i)
+      if (!fuse || chunk_order[i] != rank) order[j++] = chunk_order[i];
+    if (fuse) order[j++] = rank;
+  }
+  chunk_order = order;
 
   TensorMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -1412,7 +1514,10 @@ int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
   p.fuse_reduce = fuse ? 1 : 0;
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
-  if ((rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s, rs->shares_gpu))) return rc;
+  if (rs_phase != SH_PHASE_COMPUTE &&
+      (rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s, rs->shares_gpu || rs_phase != SH_PHASE_ALL)))
+    return rc;
+  if (rs_phase == SH_PHASE_COMM) return SH_OK;  // scatter only: reduce in a later phase call
 
   // reduction of my W staging slots in ascending source order: fused into the
   // epilogue of my own chunk's tiles (scheduled last, rs_inter_order), or a
@@ -1504,8 +1609,12 @@ int sh_signal_wait(sh_world* w, int rank, int sig, int cond, uint64_t value, voi
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t* f = sig_addr(w, *rs, rank, sig);
+  // A user-level wait must honour the world's timeout (a peer that never
+  // signals is a SynchronizationFault, not a hung stream): bounded one-thread
+  // spin that records the timeout in the error word.  The front-end wait
+  // (no SM, no timeout) stays available as SHB_WAIT_MEMOP=1.
   Driver& d = driver();
-  if (d.wait64 && (cond == 0 || cond == 2)) {
+  if (env_int("SHB_WAIT_MEMOP", 0) && d.wait64 && (cond == 0 || cond == 2)) {
     CUresult r = d.wait64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(f), value,
                           cond == 0 ? CU_STREAM_WAIT_VALUE_EQ : CU_STREAM_WAIT_VALUE_GEQ);
     if (r == CUDA_SUCCESS) return SH_OK;

@@ -74,6 +74,7 @@ def read_trace(world, rank, records_per_cta, launches):
                     "op": _KINDS.get(kind, str(kind)), "cta": cta,
                     "chunk": kind_aux & 0xFFFFFFFF if kind in (1, 2, 3) else None,
                     "item_kind": (kind_aux >> 32) & 0xFF if kind == 2 else None,
+                    "ranges": (kind_aux >> 32) & 0xFF if kind == 1 else None,
                     "stage_wait_ns": kind_aux & 0xFFFFFFFF if kind == 5 else None,
                     "tile": tile, "t0_ns": t0, "t1_ns": t1,
                 })

@@ -481,21 +481,28 @@ def test_fused_ops_exact_per_tile_config(rng, world_size, rows, n, k, cg):
         lib.sh_set_tile_config(0, 0)
 
 
-def test_unaligned_row_length_rejected():
-    # rows must be 16-byte TMA strides: n % 8 / k % 8 != 0 is an ArgumentError,
-    # never a silent CPU fallback
-    shape = ProblemShape(m=256, n=12, k=64, dtype="bfloat16")
+def test_unaligned_row_length_padded_on_device(rng):
+    # TMA rows are 16-byte multiples: a ragged n / k is zero-padded on the
+    # device by the drop-in (exact -- the padding adds zeros), never routed
+    # to a CPU fallback; the C ABI itself still refuses it
+    shape = ProblemShape(m=256, n=12, k=60, dtype="bfloat16")
     with make_world(1) as w:
         bufs = make_ag_gemm_buffers(w, shape)
+        rs_bufs = make_gemm_rs_buffers(w, ProblemShape(m=256, n=12, k=60, dtype="bfloat16"))
+        a = ints(rng, -2, 3, (256, 60))
+        b = ints(rng, -1, 2, (60, 12))
 
         def body(pe):
-            a = torch.zeros((256, 64), dtype=BF16, device=pe.torch_device)
-            b = torch.zeros((64, 12), dtype=BF16, device=pe.torch_device)
-            return ag_gemm(pe, a, b, shape, ag_order_switch(0, 1), bufs)
+            h = ag_gemm(pe, dev(a, pe), dev(b, pe), shape, ag_order_switch(0, 1), bufs)
+            y = gemm_rs(pe, dev(a, pe), dev(b, pe), shape, rs_inter_order(pe.ctx, 1, 1), rs_bufs)
+            return h, y
 
-        with pytest.raises(CollectiveFault) as info:
-            w.run(body)
-        assert isinstance(info.value.first, ArgumentError)
+        h, y = run_np(w, body)[0]
+        assert h.shape == (256, 12) and np.array_equal(h, a @ b)
+        assert y.shape == (256, 12) and np.array_equal(y, a @ b)
+    from paper_2504_19442_b200 import _lib
+
+    assert _lib.load().sh_gemm(None, None, None, 256, 12, 64, 0, None, 0, None) == _lib.SH_ERR_ARG
 
 
 def test_criterion_6_pipeline_correctness_on_gpu():

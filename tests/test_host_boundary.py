@@ -86,14 +86,47 @@ def test_problem_shape_validation():
     with pytest.raises(ArgumentError):
         ProblemShape(m=8, n=8, k=8, tile_m=-1)
     assert ProblemShape(m=8, n=8, k=8).rows_per_rank(4) == 2
-    # the tensor-core path computes in bf16/fp16; int64 (the reference default)
-    # is rejected loudly instead of silently computed on the CPU
-    with pytest.raises(ArgumentError, match="bf16/fp16"):
-        ProblemShape(m=8, n=8, k=8).torch_dtype
+    # the tensor-core path computes in bf16/fp16; int64 (the reference
+    # default) and the other widened types are staged in bf16 when exact
+    import numpy as np
     import torch
 
+    s = ProblemShape(m=8, n=6, k=12)
+    assert (s.io_dtype, s.widened, s.torch_dtype) == ("int64", True, torch.bfloat16)
+    assert (s.k_padded, s.n_padded) == (16, 8)
+    assert ProblemShape(m=8, n=8, k=8, dtype=np.float32).io_dtype == "float32"
     assert ProblemShape(m=8, n=8, k=8, dtype="bf16").torch_dtype == torch.bfloat16
+    assert not ProblemShape(m=8, n=8, k=8, dtype="bf16").widened
     assert ProblemShape(m=8, n=8, k=8, dtype="float16").dtype_code == _lib.SH_DTYPE_FP16
+    with pytest.raises(ArgumentError, match="bf16/fp16"):
+        ProblemShape(m=8, n=8, k=8, dtype="complex64").torch_dtype
+
+
+def test_serialising_tool_detection(monkeypatch):
+    from paper_2504_19442_b200.core import serialising_tool
+
+    for var in ("SHB_PHASED", "CUDA_INJECTION64_PATH", "CUDA_LAUNCH_BLOCKING"):
+        monkeypatch.delenv(var, raising=False)
+    assert not serialising_tool()
+    monkeypatch.setenv("CUDA_INJECTION64_PATH", "/opt/nvidia/nsight-compute/libInjection.so")
+    assert serialising_tool()
+    monkeypatch.setenv("SHB_PHASED", "0")
+    assert not serialising_tool()
+    monkeypatch.delenv("CUDA_INJECTION64_PATH")
+    monkeypatch.delenv("SHB_PHASED")
+    monkeypatch.setenv("CUDA_LAUNCH_BLOCKING", "1")
+    assert serialising_tool()
+
+
+def test_phase_and_subchunk_arguments_validated_without_gpu():
+    lib = _lib.load()
+    s = ctypes.c_int()
+    assert lib.sh_ag_subchunks(8192, 8192, 8, ctypes.byref(s)) == _lib.SH_OK and s.value == 4
+    assert lib.sh_ag_subchunks(8192, 8192, 1, ctypes.byref(s)) == _lib.SH_OK and s.value == 1
+    assert lib.sh_ag_subchunks(8190, 8192, 8, ctypes.byref(s)) == _lib.SH_ERR_ARG
+    order = _lib.int_array([0])
+    rc = lib.sh_gemm_rs_ex(None, 0, None, None, None, 0, 0, 0, 8, 8, 8, 0, order, 1, 7, None)
+    assert rc == _lib.SH_ERR_ARG and b"phase" in lib.sh_last_error()
 
 
 def test_world_spec_validation():
