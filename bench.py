@@ -317,6 +317,8 @@ def main():
         h_fixed = sb.ag_gemm(pe, x, w_up, ag_shape, ag_sched, agb, reset=False)
 
         def loop_ms(fn):
+            fn()  # one untimed call (first use of this operand / output set)
+            barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(k2):
@@ -328,7 +330,7 @@ def main():
         ag_ms = loop_ms(lambda: sb.ag_gemm(pe, x, w_up, ag_shape, ag_sched, agb, reset=False,
                                            out=h_buf))
         rs_ms = loop_ms(lambda: sb.gemm_rs(pe, h_fixed, w_dn, rs_shape, rs_sched, rsb,
-                                           reset=False))
+                                           reset=False, out=y_ring[1]))
     clk = clocks.summary(t_wall0, t_wall1)
 
     world.check_errors(rank)

@@ -337,7 +337,7 @@ class _HostIO:
         elif self.widened and not self.shape.io_dtype.startswith("float"):
             self.chk = torch.empty((1,), dtype=torch.float32, pin_memory=True)
         world = self.pe.world
-        if self.host and len(world.local_ranks) > 1:
+        if (self.host or self.widened) and len(world.local_ranks) > 1:
             world._host_join(self.pe)
 
     def output(self, out):
