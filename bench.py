@@ -15,7 +15,8 @@ Prints ONE JSON line on rank 0.  `value` = whole-job TFLOPS (all ranks'
 algorithmic FLOPs / max-over-ranks device time); `e2e` = the same through the
 public API with host buffers (pinned H2D of X, D2H of Y inside the timed
 region); `roofline` = the dominant kernel (the fused AG+GEMM call) against the
-measured dense-bf16 peak; `cpu_baseline` = the numpy oracle port on the host.
+measured dense-bf16 peak; `cpu_baseline` = the reference package itself
+(baseline/_ref) on the host cores.
 """
 
 from __future__ import annotations
@@ -141,52 +142,91 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle (reference arm and cpu_baseline): the numpy port of the
-# reference's ag_gemm / gemm_rs (oracle/minishmem_oracle.py), fp32 BLAS on all
-# host cores, on a row sample of the per-rank shapes.
+# The reference's CPU path (reference arm and cpu_baseline): the unmodified
+# reference package (minishmem, pure Python + numpy) installed under
+# baseline/_ref, driven through its own public API -- world.run of ag_gemm
+# then gemm_rs -- in fp32 on all host cores, on a row sample
+# of the per-rank C3/C4 shapes.  If baseline/_ref is missing, the numpy port
+# of the same algorithm (oracle/minishmem_oracle.py) stands in ("port").
+
+def _reference_package():
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "minishmem")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import minishmem  # noqa: F401
+        from minishmem import core, pipelines, swizzle
+    except Exception:  # noqa: BLE001 -- e.g. a missing dependency on the box
+        return None
+    return core, pipelines, swizzle
+
 
 def cpu_sample_step(rows_sample, rng_seed=0):
+    """(step(), flops per step, kind, teardown()) for a row sample."""
     import numpy as np
-
-    from oracle import minishmem_oracle as oracle
 
     g = np.random.default_rng(rng_seed)
     x = g.standard_normal((rows_sample, AG["k"]), dtype=np.float32)
-    w_up = g.standard_normal((AG["k"], AG["n"]), dtype=np.float32)
-    w_dn = g.standard_normal((RS["k"], RS["n"]), dtype=np.float32)
+    w_up = g.standard_normal((AG["k"], AG["n"]), dtype=np.float32) * 0.02
+    w_dn = g.standard_normal((RS["k"], RS["n"]), dtype=np.float32) * 0.02
+    fl = 2.0 * rows_sample * (AG["n"] * AG["k"] + RS["n"] * RS["k"])
+    ref = _reference_package()
+    if ref is not None:
+        core, pipes, swz = ref
+        ags = pipes.ProblemShape(m=rows_sample, n=AG["n"], k=AG["k"], dtype="float32")
+        rss = pipes.ProblemShape(m=rows_sample, n=RS["n"], k=RS["k"], dtype="float32")
+        heap = rows_sample * (AG["k"] + RS["n"]) * 4 + (1 << 20)
+        world = core.init_world(core.WorldSpec(world_size=1, heap_bytes=heap, timeout_s=600.0))
+        agb = pipes.make_ag_gemm_buffers(world, ags)
+        rsb = pipes.make_gemm_rs_buffers(world, rss)
+
+        def body(pe):
+            h = pipes.ag_gemm(pe, x, w_up, ags, swz.ag_order_switch(pe.rank, 1), agb)
+            return pipes.gemm_rs(pe, h, w_dn, rss, swz.rs_inter_order(pe.ctx, 1, 1), rsb)
+
+        return (lambda: world.run(body)), fl, "reference", world.close
+    from oracle import minishmem_oracle as oracle
 
     def step():
         (h,), _ = oracle.port_ag_gemm([x], [w_up], [[0]])
         (y,), _ = oracle.port_gemm_rs([h], [w_dn], [[0]])
         return y
 
-    return step, 2.0 * rows_sample * (AG["n"] * AG["k"] + RS["n"] * RS["k"])
+    return step, fl, "port", lambda: None
 
 
 def cpu_measure(steps, warmup, budget_s=20.0):
-    """Calibrate the row sample so one step takes ~budget_s/steps, then time."""
-    rows = 128
-    step, fl = cpu_sample_step(rows)
+    """Calibrate the row sample so one step takes ~budget_s/(steps+warmup)
+    (0.2..4 s), then time ``warmup`` untimed and ``steps`` timed steps."""
+    rows = 256
+    step, fl, kind, close = cpu_sample_step(rows)
+    step()
     t0 = time.perf_counter()
     step()
     dt = time.perf_counter() - t0
-    per_step_target = max(0.2, min(2.0, budget_s / max(1, steps)))
+    close()
+    per_step_target = max(0.2, min(4.0, budget_s / max(1, steps + warmup)))
     rows = int(max(128, min(AG["m"], rows * per_step_target / max(dt, 1e-3))) // 128 * 128)
-    step, fl = cpu_sample_step(rows)
+    step, fl, kind, close = cpu_sample_step(rows)
     for _ in range(warmup):
         step()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
+    close()
     cores = os.cpu_count()
     threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+    what = ("the reference package minishmem (baseline/_ref, unmodified): world.run of "
+            "ag_gemm then gemm_rs" if kind == "reference" else
+            "numpy port of the reference (oracle/minishmem_oracle.py): ag_gemm + gemm_rs")
     return {
         "value": fl / dt / 1e12, "unit": "TFLOPS",
-        "cores": int(threads) if threads else cores, "kind": "port",
-        "sample": (f"oracle port (numpy fp32 BLAS) of ag_gemm+gemm_rs at W=1 on {rows} of "
-                   f"{AG['m']} rows of the C3/C4 per-rank shapes, {steps} steps, "
-                   f"{dt * 1e3:.1f} ms/step"),
+        "cores": int(threads) if threads else cores, "kind": kind,
+        "sample": (f"{what}, fp32, W=1, {rows} of {AG['m']} rows of the C3/C4 per-rank shapes, "
+                   f"{warmup} warm-up + {steps} timed steps, {dt * 1e3:.1f} ms/step"),
         "ms_per_step": dt * 1e3,
     }
 
@@ -194,9 +234,8 @@ def cpu_measure(steps, warmup, budget_s=20.0):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 10))
-    warm = max(0, min(args.warmup, 1))
-    cb = cpu_measure(steps, warm, budget_s=30.0)
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    cb = cpu_measure(steps, warm, budget_s=150.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "TFLOPS",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": cb["ms_per_step"],
@@ -205,8 +244,6 @@ def run_reference(args, rank, world):
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "TFLOPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "note": ("reference = numpy restatement of minishmem ag_gemm/gemm_rs (the reference "
-                 "package is pure Python+numpy and cannot travel to the GPU box)"),
     }
     print(json.dumps(line), flush=True)
 
@@ -473,7 +510,7 @@ def main():
 
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        cb = cpu_measure(steps=5, warmup=1, budget_s=15.0)
+        cb = cpu_measure(steps=5, warmup=1, budget_s=20.0)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     # ------------------------------------------------------------- roofline
