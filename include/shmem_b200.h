@@ -217,6 +217,17 @@ int sh_set_dynamic_tiles(int mode);
 /* Launch config chosen for a problem (for the bench's roofline bookkeeping). */
 int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid);
 
+/* Single-GPU TP proxy (measurement only; no reference counterpart): treat
+ * `rank` as the only rank on its device (full persistent grid, overlapped
+ * side-stream pushes) while its peers are emulated by feeder streams that do
+ * not launch GEMMs; solo=0 restores the device-sharing bookkeeping. */
+int sh_set_rank_solo(sh_world* w, int rank, int solo);
+/* Stamp %globaltimer into the device word `origin` (stream-ordered). */
+int sh_pace_mark(void* origin, void* stream);
+/* Hold `stream` until %globaltimer >= *origin + delta_ns (one thread, no smem:
+ * co-resides with a persistent GEMM CTA).  delta_ns <= 10 s. */
+int sh_pace_wait(const void* origin, uint64_t delta_ns, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

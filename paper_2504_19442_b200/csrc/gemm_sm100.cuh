@@ -1137,4 +1137,18 @@ __global__ void flag_wait_kernel(const uint64_t* flag, uint64_t target, int* err
   if (threadIdx.x == 0) spin_geq(flag, target, err, timeout_ns, 4);
 }
 
+// Pacing for the single-GPU TP proxy (bench.py tp8_proxy): an emulated peer's
+// feeder stream stamps a time origin once, then holds each transfer back until
+// origin + delta -- the arrival time the same bytes would have over NVLink.
+// One thread, no shared memory: it sits next to a persistent GEMM CTA.
+__global__ void pace_mark_kernel(uint64_t* origin) {
+  if (threadIdx.x == 0) *origin = globaltimer();
+}
+
+__global__ void pace_wait_kernel(const uint64_t* origin, uint64_t delta_ns) {
+  if (threadIdx.x != 0) return;
+  const uint64_t until = *reinterpret_cast<const volatile uint64_t*>(origin) + delta_ns;
+  while (globaltimer() < until) __nanosleep(500);
+}
+
 }  // namespace shb

@@ -505,7 +505,9 @@ int preload_kernels(int dev) {
                          reinterpret_cast<const void*>(flag_store_kernel),
                          reinterpret_cast<const void*>(flag_store_list_kernel),
                          reinterpret_cast<const void*>(flag_wait_kernel),
-                         reinterpret_cast<const void*>(flag_fill_kernel)};
+                         reinterpret_cast<const void*>(flag_fill_kernel),
+                         reinterpret_cast<const void*>(pace_mark_kernel),
+                         reinterpret_cast<const void*>(pace_wait_kernel)};
   for (const void* f : small) {
     cudaFuncAttributes a;
     CUDA_TRY(cudaFuncGetAttributes(&a, f));
@@ -1060,6 +1062,43 @@ int sh_set_schedule_config(int stream_k, int group_m) {
 int sh_set_dynamic_tiles(int mode) {
   if (mode < -1 || mode > 1) return fail(SH_ERR_ARG, "mode must be -1, 0 or 1");
   g_dynamic = mode;
+  return SH_OK;
+}
+
+int sh_set_rank_solo(sh_world* w, int rank, int solo) {
+  RankState* rs = rank_of(w, rank);
+  if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
+  if (solo) {
+    rs->shares_gpu = false;
+    rs->ranks_on_device = 1;
+    return SH_OK;
+  }
+  rs->ranks_on_device = 1;
+  rs->shares_gpu = false;
+  for (int q = 0; q < w->world; ++q)
+    if (q != rank && w->r[q].device == rs->device && w->r[q].rank >= 0) {
+      rs->shares_gpu = true;
+      rs->ranks_on_device++;
+    }
+  return SH_OK;
+}
+
+int sh_pace_mark(void* origin, void* stream) {
+  if (!origin || (reinterpret_cast<uintptr_t>(origin) & 7))
+    return fail(SH_ERR_ARG, "origin must be an 8-byte aligned device word");
+  pace_mark_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint64_t*>(origin));
+  CUDA_TRY(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_pace_wait(const void* origin, uint64_t delta_ns, void* stream) {
+  if (!origin || (reinterpret_cast<uintptr_t>(origin) & 7))
+    return fail(SH_ERR_ARG, "origin must be an 8-byte aligned device word");
+  if (delta_ns > 10000000000ull) return fail(SH_ERR_ARG, "delta %llu ns above 10 s",
+                                             (unsigned long long)delta_ns);
+  pace_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint64_t*>(origin), delta_ns);
+  CUDA_TRY(cudaGetLastError());
   return SH_OK;
 }
 
