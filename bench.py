@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-unfused", action="store_true")
     p.add_argument("--no-sweep", action="store_true", help="skip the C5 TP/M sweep")
+    p.add_argument("--no-proxy", action="store_true", help="skip the single-GPU TP=8 proxy")
     return p.parse_args()
 
 
@@ -524,6 +525,17 @@ def main():
             world.check_errors(rank)
         except Exception as e:  # noqa: BLE001 -- the sweep must never cost the headline line
             sweep = {"error": f"{type(e).__name__}: {e}"[:300]}
+    proxy = None
+    if rank == 0 and N == 1 and not args.no_proxy:
+        # rank 0 of TP=8 at the C3/C4 per-rank shapes, peers emulated on this
+        # GPU (tp_proxy.py); not a scaling number -- SCALE runs measure N>1
+        try:
+            import tp_proxy
+
+            proxy = tp_proxy.run(W=8, iters=20, peak_tflops=burst, ab=False)
+            proxy["label"] = "tp8_proxy"
+        except Exception as e:  # noqa: BLE001 -- the proxy must never cost the headline line
+            proxy = {"label": "tp8_proxy", "error": f"{type(e).__name__}: {e}"[:300]}
     dom_ms = ag_ms
     achieved = flops(AG) / (dom_ms * 1e-3) / 1e12
     # the roofline call is timed right after K back-to-back steps: under the
@@ -564,6 +576,7 @@ def main():
                 "frac_of_pcie_floor": pcie_ms / e2e_ms},
         "unfused_baseline": unfused,
         "sweep": sweep,
+        "tp8_proxy": proxy,
         "cpu_baseline": cpu,
         "gpu_launches": args.steps * 2,
         "gpu_launches_note": ("per step: gemm_tp_kernel<MODE_AG> + gemm_tp_kernel<MODE_RS> "

@@ -222,12 +222,14 @@ int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, in
  * side-stream pushes) while its peers are emulated by feeder streams that do
  * not launch GEMMs; solo=0 restores the device-sharing bookkeeping. */
 int sh_set_rank_solo(sh_world* w, int rank, int solo);
-/* Stamp %globaltimer into the device word `origin` (stream-ordered). */
-int sh_pace_mark(void* origin, void* stream);
-/* Hold `stream` until %globaltimer >= *origin + delta_ns (one thread, no smem:
- * co-resides with a persistent GEMM CTA).  delta_ns <= 10 s. */
-int sh_pace_wait(const void* origin, uint64_t delta_ns, void* stream);
-
+/* Stream memory operations on any 8-byte word (device memory, or pinned host
+ * memory under UVA): a front-end write / a GEQ wait, no SM involved. */
+int sh_stream_write_word(void* word, uint64_t value, void* stream);
+int sh_stream_wait_word(const void* word, uint64_t value, void* stream);
+/* Host pacer: spin until *origin >= origin_value, then store tick_base+i+1
+ * into *tick at origin + deltas_ns[i] (host monotonic clock).  Blocking. */
+int sh_pace_host(const void* origin, uint64_t origin_value, void* tick, uint64_t tick_base,
+                 const uint64_t* deltas_ns, int n, double timeout_s);
 #ifdef __cplusplus
 }
 #endif

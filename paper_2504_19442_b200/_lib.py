@@ -116,8 +116,10 @@ SIGNATURES = {
     "sh_query_tile_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int_p,
                                             _c_int_p, _c_int_p]),
     "sh_set_rank_solo": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
-    "sh_pace_mark": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
-    "sh_pace_wait": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]),
+    "sh_stream_write_word": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]),
+    "sh_stream_wait_word": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]),
+    "sh_pace_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
+                                    ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_double]),
 }
 
 _lock = threading.Lock()

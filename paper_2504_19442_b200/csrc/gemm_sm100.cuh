@@ -52,6 +52,7 @@ struct TileParams {
   uint64_t rs_target;                 // RS: epoch * rows * n, a chunk fully delivered
   const uint16_t* staging_local;      // RS: my staging buffer (W slots of rows x n)
   int fuse_reduce;                    // RS: reduce my chunk in the epilogue of its tiles
+  uint16_t* out_rows;                 // RS: the reduced output rows (rows x n, row-major)
   int copy_own;                       // AG: store own-chunk A stages into gathered[rank]
   // optional timeline: per CTA `trace_cap` records of 4 u64 {kind|aux, t0, t1, tile}
   // (%globaltimer ns); producer records fill from the front, epilogue (warp 2)
@@ -332,6 +333,66 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi, bool fp16) {
   }
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Fused ReduceScatter reduction of one epilogue warp's 32 rows x BN columns
+// of my own chunk (see the MODE_RS epilogue): lane l owns columns
+// [n0 + 8l, n0 + 8l + 8) of every row, so one warp-wide load reads 512
+// contiguous bytes of one source's row; kRedRows rows x up to 8 sources are
+// in flight per lane before the first add.  Sum in ascending source order
+// from +0.0f in fp32, rounded once (reference collectives.py:163-171).
+template <int BN, bool FP16>
+__device__ __forceinline__ void reduce_rows(const TileParams& p, int row0, int n0, uint32_t lane) {
+  constexpr int kRedRows = 4;
+  constexpr int kGroup = 8;
+  const int col = n0 + (int)lane * 8;
+  if ((int)lane * 8 >= BN || col + 8 > p.n) return;
+  const size_t slot_elems = (size_t)p.rows * p.n;
+#pragma unroll 1
+  for (int r0 = 0; r0 < 32; r0 += kRedRows) {
+    float acc[kRedRows][8];
+#pragma unroll
+    for (int r = 0; r < kRedRows; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[r][e] = 0.f;
+#pragma unroll 1
+    for (int s0 = 0; s0 < p.world; s0 += kGroup) {
+      uint4 v[kRedRows][kGroup];
+#pragma unroll
+      for (int r = 0; r < kRedRows; ++r) {
+        const int grow = row0 + r0 + r;
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+          const int s = s0 + g;
+          v[r][g] = (grow < p.rows && s < p.world)
+                        ? __ldcg(reinterpret_cast<const uint4*>(
+                              p.staging_local + (size_t)s * slot_elems + (size_t)grow * p.n + col))
+                        : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kRedRows; ++r)
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+          if (s0 + g >= p.world) break;
+          const uint32_t wv[4] = {v[r][g].x, v[r][g].y, v[r][g].z, v[r][g].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = unpack2(wv[e], FP16);
+            acc[r][2 * e] += f.x;
+            acc[r][2 * e + 1] += f.y;
+          }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kRedRows; ++r) {
+      const int grow = row0 + r0 + r;
+      if (grow < p.rows)
+        *reinterpret_cast<uint4*>(p.out_rows + (size_t)grow * p.n + col) =
+            make_uint4(pack2(acc[r][0], acc[r][1], FP16), pack2(acc[r][2], acc[r][3], FP16),
+                       pack2(acc[r][4], acc[r][5], FP16), pack2(acc[r][6], acc[r][7], FP16));
+    }
+  }
 }
 
 constexpr int kThreads = 224;  // 7 warps: producer, MMA, 4 epilogue, own-slot copier
@@ -638,7 +699,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     uint8_t* stg = sEpi + (warp - 2) * C::EPI_NBUF * C::EPI_BUF;
     int buf = 0;
-    bool paired = false;   // staging ring currently used as {own, sum} pairs
     int it = 0;
     uint32_t freed = 0;    // RS: destinations observed free for this epoch
     bool peers_in = false;  // RS fused: every peer's contribution to my chunk landed
@@ -684,6 +744,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (tracer) trace_rec(p, trace_slot++, (3ull << 56) | chunk, tw0, globaltimer(), w.t);
         peers_in = true;
+      }
+      if (MODE == MODE_RS && fused_own && p.world > 1) {
+        // Peers' rows of this tile are in memory (peers_in): pull this
+        // warp's 32 rows of every peer slot into L2 while the tile's MMA is
+        // still running, so the reduction below reads L2 instead of waiting
+        // on DRAM (one bulk prefetch per row and source, lanes in parallel).
+        const int cols = min(BN, p.n - n0);
+        for (int i = (int)lane; i < 32 * p.world; i += 32) {
+          const int s = i >> 5, r = row + (i & 31);
+          if (s != p.rank && r < p.rows && cols > 0)
+            prefetch_l2_bulk(p.staging_local + (size_t)s * slot_elems + (size_t)r * p.n + n0,
+                             (uint32_t)cols * 2u);
+        }
       }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
@@ -767,16 +840,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int xcol = n0 + j * C::SUB;
         const int swz = (lane >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk ^= row bits 1..2
         // a world of one reduces a single slot: out == staging[0] bit for bit,
-        // so both stores are issued from one staging buffer
+        // so both stores are issued from one staging buffer; at W > 1 my own
+        // chunk's tile goes to staging[rank] like any other chunk's and is
+        // reduced below, once its rows are in memory
         const bool dual = fused_own && p.world == 1;
-        if (!fused_own || dual) {
+        {
           // 4-deep ring of staging buffers: at most 3 stores still reading smem
-          // (drain fully when coming from the paired layout of fused tiles)
-          if (lane == 0) {
-            if (paired) bulk_wait_read<0>();
-            else bulk_wait_read<C::EPI_NBUF - 1>();
-          }
-          paired = false;
+          if (lane == 0) bulk_wait_read<C::EPI_NBUF - 1>();
           __syncwarp();
           uint8_t* sb = stg + buf * C::EPI_BUF;
           uint8_t* rowp = sb + lane * 64;
@@ -796,71 +866,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_commit();
           }
           buf = (buf + 1) % C::EPI_NBUF;
-        } else {
-          // fused reduction of my own chunk: out = sum_{s ascending} slot_s in
-          // fp32 with slot_rank = this tile rounded to bf16 -- the exact
-          // arithmetic of the separate reduction kernel (and of the reference's
-          // ascending `acc +=`), minus one HBM round trip of every slot.
-          float acc[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) acc[e] = 0.f;
-          const int grow = row + (int)lane;
-          const bool row_ok = grow < p.rows;
-          for (int s = 0; s < p.world; ++s) {
-            if (s == p.rank) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                float2 f = unpack2(pk[e], FP16);
-                acc[2 * e] += f.x;
-                acc[2 * e + 1] += f.y;
-              }
-            } else if (row_ok) {
-              const uint4* src = reinterpret_cast<const uint4*>(
-                  p.staging_local + (size_t)s * slot_elems + (size_t)grow * p.n + xcol);
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                if (xcol + c * 8 < p.n) {
-                  uint4 w = src[c];
-                  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    float2 f = unpack2(wv[e], FP16);
-                    acc[c * 8 + 2 * e] += f.x;
-                    acc[c * 8 + 2 * e + 1] += f.y;
-                  }
-                }
-              }
-            }
-          }
-          // buffer pairs {0,1} / {2,3} alternate; one commit group per pair
-          if (lane == 0) {
-            if (paired) bulk_wait_read<1>();
-            else bulk_wait_read<0>();
-          }
-          paired = true;
-          __syncwarp();
-          const int pair = (buf >> 1) & 1;
-          uint8_t* own_b = stg + (2 * pair) * C::EPI_BUF;
-          uint8_t* sum_b = stg + (2 * pair + 1) * C::EPI_BUF;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int so = lane * 64 + ((c ^ swz) << 4);
-            *reinterpret_cast<uint4*>(own_b + so) =
-                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            *reinterpret_cast<uint4*>(sum_b + so) = make_uint4(
-                pack2(acc[8 * c + 0], acc[8 * c + 1], FP16), pack2(acc[8 * c + 2], acc[8 * c + 3], FP16),
-                pack2(acc[8 * c + 4], acc[8 * c + 5], FP16), pack2(acc[8 * c + 6], acc[8 * c + 7], FP16));
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            // staging slot `rank` (layout) and the reduced output rows
-            tma_store_2d_hint(&maps.out[chunk], own_b, xcol, row, p.l2_hint_store);
-            tma_store_3d_hint(&maps.c, sum_b, xcol, row, 0, p.l2_hint_store);
-            bulk_commit();
-          }
-          buf = (pair ^ 1) * 2;
         }
+      }
+      if (MODE == MODE_RS && fused_own && p.world > 1) {
+        // the reduce side of rs_intra_streams (collectives.py:163-171) for
+        // this warp's 32 rows of the tile: out = sum_{s ascending} slot_s in
+        // fp32, slot_rank being the bf16 rows just stored -- the arithmetic
+        // of the separate reduction kernel and of the reference's ascending
+        // `acc +=`.  Row-contiguous 16-byte loads (a warp reads 512 B of one
+        // row per source) with kRedRows rows x every source in flight: the
+        // per-lane-row loads of the accumulator layout were DRAM-latency
+        // bound (~48 us per 256x256 tile at W=8).
+        const uint64_t tr0 = tracer ? globaltimer() : 0;
+        if (lane == 0) {
+          bulk_wait<0>();
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+        const uint64_t tr1 = tracer ? globaltimer() : 0;
+        reduce_rows<BN, FP16>(p, row, n0, lane);
+        if (tracer)  // kind 6: own-chunk reduction, aux = store-drain part (ns)
+          trace_rec(p, trace_slot++, (6ull << 56) | ((tr1 - tr0) & 0xFFFFFFFFull), tr0, globaltimer(),
+                    w.t);
       }
       if (tracer)
         trace_rec(p, trace_slot++, (2ull << 56) | ((uint64_t)w.kind << 32) | (uint64_t)chunk, t_acc,
@@ -1135,20 +1162,6 @@ __global__ void flag_fill_kernel(uint64_t* words, int count, uint64_t value) {
 __global__ void flag_wait_kernel(const uint64_t* flag, uint64_t target, int* err,
                                  uint64_t timeout_ns) {
   if (threadIdx.x == 0) spin_geq(flag, target, err, timeout_ns, 4);
-}
-
-// Pacing for the single-GPU TP proxy (bench.py tp8_proxy): an emulated peer's
-// feeder stream stamps a time origin once, then holds each transfer back until
-// origin + delta -- the arrival time the same bytes would have over NVLink.
-// One thread, no shared memory: it sits next to a persistent GEMM CTA.
-__global__ void pace_mark_kernel(uint64_t* origin) {
-  if (threadIdx.x == 0) *origin = globaltimer();
-}
-
-__global__ void pace_wait_kernel(const uint64_t* origin, uint64_t delta_ns) {
-  if (threadIdx.x != 0) return;
-  const uint64_t until = *reinterpret_cast<const volatile uint64_t*>(origin) + delta_ns;
-  while (globaltimer() < until) __nanosleep(500);
 }
 
 }  // namespace shb

@@ -147,6 +147,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 // ---------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor)
 
+// Bulk L2 prefetch of `bytes` (multiple of 16) contiguous bytes at a
+// 16-byte aligned global address; no completion to wait for.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
 }

@@ -169,17 +169,19 @@ void sk_late_partition(const Cfg& c, TileParams& p, int world, size_t chunk_byte
   p.sk_late_units = (int)d;
 }
 
-// Sub-chunk count of the AG pushes (see sh_ag_gemm_ex): a late cluster whose
-// first tile sits in the first remote chunk waits for its own row range
-// rather than the whole shard (C3/TP=8: 4 MB, ~5 us at 770 GB/s, instead of
-// 16 MB).  Small shards stay whole (the per-range flag write is a stream
-// memory op, ~2 us of copy-engine issue each).  SHB_AG_SUB=S forces S.
+// Sub-chunk count of the AG pushes (see sh_ag_gemm_ex): S > 1 splits every
+// pushed shard into S row ranges, each released by its own flag write.  Off
+// by default: measured on the TP=8 proxy (tp_proxy.py), every stream memory
+// op with its memory barrier costs ~7 us of front-end time, so 4 ranges per
+// shard stretch the push pipeline by ~3x that per chunk, while the clusters
+// that open on a remote chunk need rows from all of its m-blocks anyway (the
+// raster walks the chunk's m-blocks first).  SHB_AG_SUB=S forces S.
 int ag_subchunks(int rows, int k, int world) {
+  (void)rows;
+  (void)k;
   if (world <= 1) return 1;
   if (const char* e = getenv("SHB_AG_SUB")) return std::max(1, std::min(64, atoi(e)));
-  const double bytes = (double)rows * k * 2;
-  if (bytes < 8.0 * (1 << 20)) return 1;
-  return std::max(1, std::min(4, rows / 256));
+  return 1;
 }
 
 // fp32 partial workspace for the stream-K tail of one stream of launches.
@@ -505,9 +507,7 @@ int preload_kernels(int dev) {
                          reinterpret_cast<const void*>(flag_store_kernel),
                          reinterpret_cast<const void*>(flag_store_list_kernel),
                          reinterpret_cast<const void*>(flag_wait_kernel),
-                         reinterpret_cast<const void*>(flag_fill_kernel),
-                         reinterpret_cast<const void*>(pace_mark_kernel),
-                         reinterpret_cast<const void*>(pace_wait_kernel)};
+                         reinterpret_cast<const void*>(flag_fill_kernel)};
   for (const void* f : small) {
     cudaFuncAttributes a;
     CUDA_TRY(cudaFuncGetAttributes(&a, f));
@@ -730,6 +730,17 @@ int store_flags(cudaStream_t s, uint64_t* const* ptrs, int count, uint64_t value
   flag_store_list_kernel<<<1, 32, 0, s>>>(l, nk, value);
   CUDA_TRY(cudaGetLastError());
   return SH_OK;
+}
+
+// Copies of the push / put / get paths.  Across devices (peer access over
+// NVLink) cudaMemcpyAsync runs on the copy engines and overlaps a persistent
+// GEMM.  Within one device the driver may run it as a copy kernel on the SMs
+// (measured with the TP proxy: a feeder copy stalled behind a persistent GEMM
+// whose CTAs left no register room for it), which is why ranks sharing a GPU
+// push on the caller's stream ahead of their GEMM.
+cudaError_t ce_copy(void* dst, const void* src, size_t nbytes, cudaStream_t s) {
+  if (nbytes == 0) return cudaSuccess;
+  return cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, s);
 }
 
 // Each call bakes its epoch (and the stream-K workspace epoch) into the
@@ -1083,24 +1094,63 @@ int sh_set_rank_solo(sh_world* w, int rank, int solo) {
   return SH_OK;
 }
 
-int sh_pace_mark(void* origin, void* stream) {
-  if (!origin || (reinterpret_cast<uintptr_t>(origin) & 7))
-    return fail(SH_ERR_ARG, "origin must be an 8-byte aligned device word");
-  pace_mark_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint64_t*>(origin));
-  CUDA_TRY(cudaGetLastError());
+// Stream memory operations on an arbitrary 8-byte word (device, or pinned
+// host memory under UVA): executed by the GPU front end, no SM involved.
+int sh_stream_write_word(void* word, uint64_t value, void* stream) {
+  if (!word || (reinterpret_cast<uintptr_t>(word) & 7))
+    return fail(SH_ERR_ARG, "word must be 8-byte aligned");
+  Driver& d = driver();
+  if (!d.write64) return fail(SH_ERR_CUDA, "cuStreamWriteValue64 unavailable");
+  CUresult r = d.write64(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(word),
+                         value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(SH_ERR_CUDA, "cuStreamWriteValue64: error %d", (int)r);
   return SH_OK;
 }
 
-int sh_pace_wait(const void* origin, uint64_t delta_ns, void* stream) {
-  if (!origin || (reinterpret_cast<uintptr_t>(origin) & 7))
-    return fail(SH_ERR_ARG, "origin must be an 8-byte aligned device word");
-  if (delta_ns > 10000000000ull) return fail(SH_ERR_ARG, "delta %llu ns above 10 s",
-                                             (unsigned long long)delta_ns);
-  pace_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint64_t*>(origin), delta_ns);
-  CUDA_TRY(cudaGetLastError());
+int sh_stream_wait_word(const void* word, uint64_t value, void* stream) {
+  if (!word || (reinterpret_cast<uintptr_t>(word) & 7))
+    return fail(SH_ERR_ARG, "word must be 8-byte aligned");
+  Driver& d = driver();
+  if (!d.wait64) return fail(SH_ERR_CUDA, "cuStreamWaitValue64 unavailable");
+  CUresult r = d.wait64(reinterpret_cast<CUstream>(stream),
+                        reinterpret_cast<CUdeviceptr>(const_cast<void*>(word)), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(SH_ERR_CUDA, "cuStreamWaitValue64: error %d", (int)r);
   return SH_OK;
 }
+
+// Host pacer of the TP proxy (tp_proxy.py): spin until a stream has written
+// `origin_value` (or more) into the pinned word `origin` -- the moment a
+// paced call starts -- then store tick_base + i + 1 into the pinned word
+// `tick` at origin + deltas_ns[i] on the host's monotonic clock.  A feeder
+// stream gates each flag release on its tick (sh_stream_wait_word): no SM
+// and no copy engine is involved, so the kernel under test shares nothing
+// with the pacing.  Blocking; call it from its own thread (ctypes drops the
+// GIL around the call).
+int sh_pace_host(const void* origin, uint64_t origin_value, void* tick, uint64_t tick_base,
+                 const uint64_t* deltas_ns, int n, double timeout_s) {
+  if (!origin || !tick || n < 0 || (n > 0 && !deltas_ns)) return fail(SH_ERR_ARG, "null pacer argument");
+  auto* o = static_cast<const volatile uint64_t*>(origin);
+  auto* t = static_cast<volatile uint64_t*>(tick);
+  auto now = [] {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
+  };
+  const uint64_t limit = (uint64_t)((timeout_s > 0 ? timeout_s : 10.0) * 1e9);
+  const uint64_t t_in = now();
+  while (*o < origin_value)
+    if (now() - t_in > limit) return fail(SH_ERR_TIMEOUT, "pacer origin never written");
+  const uint64_t t0 = now();
+  for (int i = 0; i < n; ++i) {
+    while (now() - t0 < deltas_ns[i]) {
+    }
+    std::atomic_thread_fence(std::memory_order_release);
+    *t = tick_base + (uint64_t)i + 1;
+  }
+  return SH_OK;
+}
+
 
 int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, int* grid) {
   int dev = 0;
@@ -1315,16 +1365,15 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
       for (int j = 0; j < S_eff; ++j) {
         const size_t r0 = (size_t)j * sub_rows;
         const size_t nr = std::min<size_t>(sub_rows, rows - r0);
-        CUDA_TRY(cudaMemcpyAsync(dst + r0 * row_bytes, static_cast<const char*>(a_shard) + r0 * row_bytes,
-                                 nr * row_bytes, cudaMemcpyDeviceToDevice, cs));
+        CUDA_TRY(ce_copy(dst + r0 * row_bytes, static_cast<const char*>(a_shard) + r0 * row_bytes,
+                         nr * row_bytes, cs));
         if ((rc = store_flags(cs, &f, 1, (epoch - 1) * (uint64_t)S_eff + j + 1))) return rc;
       }
     }
     // own slot: written by the GEMM's idle epilogue warps from L2-hot rows
     // (own_dst below); the copy-engine path stays available for A/B checks
     if (own_by_ce)
-      CUDA_TRY(cudaMemcpyAsync(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes,
-                               cudaMemcpyDeviceToDevice, cs));
+      CUDA_TRY(ce_copy(own_gathered + (size_t)rank * chunk_bytes, a_shard, chunk_bytes, cs));
   }
   if (!do_compute) return SH_OK;
 
@@ -1550,6 +1599,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   p.rs_mine = sig_addr(w, *rs, rank, reduction_base);
   p.rs_target = target;
   p.staging_local = staging;
+  p.out_rows = static_cast<uint16_t*>(out);
   p.fuse_reduce = fuse ? 1 : 0;
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
@@ -1600,8 +1650,8 @@ int sh_putmem(sh_world* w, int rank, int peer, size_t dst_off, const void* src, 
   if (nbytes == 0) return SH_OK;
   if (!src) return fail(SH_ERR_ARG, "null source");
   CUDA_TRY(cudaSetDevice(rs->device));
-  CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(rs->peer[peer]) + dst_off, src, nbytes,
-                           cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  CUDA_TRY(ce_copy(static_cast<char*>(rs->peer[peer]) + dst_off, src, nbytes,
+                   static_cast<cudaStream_t>(stream)));
   return SH_OK;
 }
 
@@ -1617,8 +1667,8 @@ int sh_getmem(sh_world* w, int rank, void* dst, int peer, size_t src_off, size_t
   if (nbytes == 0) return SH_OK;
   if (!dst) return fail(SH_ERR_ARG, "null destination");
   CUDA_TRY(cudaSetDevice(rs->device));
-  CUDA_TRY(cudaMemcpyAsync(dst, static_cast<char*>(rs->peer[peer]) + src_off, nbytes,
-                           cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  CUDA_TRY(ce_copy(dst, static_cast<char*>(rs->peer[peer]) + src_off, nbytes,
+                   static_cast<cudaStream_t>(stream)));
   return SH_OK;
 }
 

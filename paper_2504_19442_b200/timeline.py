@@ -21,7 +21,8 @@ from collections import defaultdict
 
 from . import _lib
 
-_KINDS = {1: "chunk_wait", 2: "tile_epilogue", 3: "peer_wait", 4: "cta", 5: "mma_item"}
+_KINDS = {1: "chunk_wait", 2: "tile_epilogue", 3: "peer_wait", 4: "cta", 5: "mma_item",
+          6: "own_reduce"}
 _MODES = {0: "ag_gemm", 1: "gemm_rs"}
 
 
@@ -76,6 +77,7 @@ def read_trace(world, rank, records_per_cta, launches):
                     "item_kind": (kind_aux >> 32) & 0xFF if kind == 2 else None,
                     "ranges": (kind_aux >> 32) & 0xFF if kind == 1 else None,
                     "stage_wait_ns": kind_aux & 0xFFFFFFFF if kind == 5 else None,
+                    "drain_ns": kind_aux & 0xFFFFFFFF if kind == 6 else None,
                     "tile": tile, "t0_ns": t0, "t1_ns": t1,
                 })
     return events

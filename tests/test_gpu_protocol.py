@@ -138,7 +138,9 @@ def test_default_subchunk_policy():
 
     lib = _lib.load()
     s = ctypes.c_int()
-    assert lib.sh_ag_subchunks(8192, 8192, 8, ctypes.byref(s)) == 0 and s.value == 4  # C3 TP=8
+    # one flag per shard by default (tp_proxy.py: every flag write costs ~7 us
+    # of front-end time); SHB_AG_SUB forces sub-chunks
+    assert lib.sh_ag_subchunks(8192, 8192, 8, ctypes.byref(s)) == 0 and s.value == 1  # C3 TP=8
     assert lib.sh_ag_subchunks(8192, 8192, 1, ctypes.byref(s)) == 0 and s.value == 1
     assert lib.sh_ag_subchunks(1024, 8192, 8, ctypes.byref(s)) == 0 and s.value == 1  # 2 MB
 

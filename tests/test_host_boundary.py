@@ -121,7 +121,7 @@ def test_serialising_tool_detection(monkeypatch):
 def test_phase_and_subchunk_arguments_validated_without_gpu():
     lib = _lib.load()
     s = ctypes.c_int()
-    assert lib.sh_ag_subchunks(8192, 8192, 8, ctypes.byref(s)) == _lib.SH_OK and s.value == 4
+    assert lib.sh_ag_subchunks(8192, 8192, 8, ctypes.byref(s)) == _lib.SH_OK and s.value == 1
     assert lib.sh_ag_subchunks(8192, 8192, 1, ctypes.byref(s)) == _lib.SH_OK and s.value == 1
     assert lib.sh_ag_subchunks(8190, 8192, 8, ctypes.byref(s)) == _lib.SH_ERR_ARG
     order = _lib.int_array([0])
