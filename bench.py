@@ -280,7 +280,8 @@ def main():
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     N = world_env
-    heap = (AG["m"] * AG["k"] + RS["m"] * RS["n"]) * 2 + (64 << 20)
+    # AG gather + RS staging + the comm probe's own gather buffer (N>1) + slack
+    heap = (2 * AG["m"] * AG["k"] + RS["m"] * RS["n"]) * 2 + (64 << 20)
     if not args.no_sweep:
         heap += sweep_heap_bytes(world_env)
     if N > 1:
@@ -372,6 +373,8 @@ def main():
     clk = clocks.summary(t_wall0, t_wall1)
 
     world.check_errors(rank)
+    comm = measure_comm(sb, world, pe, N, rank, x, step, stream, barrier, max_over_ranks) \
+        if N > 1 else None
 
     # ------------------------------------------------------------- baselines
     # measured right after our K-step block, before the PCIe-bound e2e phase
@@ -577,6 +580,7 @@ def main():
         "unfused_baseline": unfused,
         "sweep": sweep,
         "tp8_proxy": proxy,
+        "comm": comm,
         "cpu_baseline": cpu,
         "gpu_launches": args.steps * 2,
         "gpu_launches_note": ("per step: gemm_tp_kernel<MODE_AG> + gemm_tp_kernel<MODE_RS> "
@@ -592,6 +596,61 @@ def main():
 
 
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def measure_comm(sb, world, pe, N, rank, x, step, stream, barrier, max_over_ranks, reps=10):
+    """N>1: achieved NVLink rate of the AG push (the comm half on its own:
+    allgather_push_intra of this rank's C3 shard into every peer, copy
+    engine, waits for every slot) and the exposed communication of one fused
+    step from the device timeline (CTA time spent waiting on remote chunks /
+    peers' rows), both max over ranks."""
+    import torch
+
+    from paper_2504_19442_b200 import collectives, timeline
+
+    out = {}
+    try:
+        with torch.cuda.stream(stream):
+            agb_buf = world.alloc_symmetric(N * x.numel() * 2, align=1024)
+            sigs = world.alloc_signals(N)
+            ts = []
+            for i in range(reps + 2):
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                collectives.allgather_push_intra(pe, agb_buf, sigs, x, wait_all=True, reset=True)
+                e1.record(stream)
+                barrier()
+                if i >= 2:
+                    ts.append(e0.elapsed_time(e1))
+            t_ms = max_over_ranks(statistics.median(ts))
+            moved = (N - 1) * x.numel() * 2
+            out["ag_push"] = {"bytes_per_rank_each_way": moved, "ms": t_ms,
+                              "gbs_per_direction": moved / (t_ms * 1e-3) / 1e9,
+                              "frac_of_900": moved / (t_ms * 1e-3) / 900e9,
+                              "how": "allgather_push_intra of the C3 shard (copy engine, one flag per "
+                                     "slot), all ranks at once, median of 10, max over ranks"}
+    except Exception as e:  # noqa: BLE001 -- the comm probe must never cost the headline line
+        out["ag_push"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    try:
+        with torch.cuda.stream(stream):
+            world.start_trace()
+            step(x)
+            barrier()
+            ev = world.stop_trace()
+        summ = timeline.exposed_comm(ev)
+        for kern in ("ag_gemm", "gemm_rs"):
+            rows_ = [s_ for s_ in summ if s_["kernel"] == kern]
+            if rows_:
+                r_ = rows_[-1]
+                out[kern] = {"exposed_wait_max_us": max_over_ranks(r_["wait_max_us"]),
+                             "exposed_wait_mean_us": max_over_ranks(r_["wait_mean_us"]),
+                             "span_us": max_over_ranks(r_["span_us"] or 0.0)}
+        out["exposed_how"] = ("device timeline of one traced step: per CTA, time spent waiting "
+                              "for a remote chunk (AG) / peers' rows (fused RS); max over ranks")
+    except Exception as e:  # noqa: BLE001
+        out["exposed_error"] = f"{type(e).__name__}: {e}"[:300]
+    return out
 
 # C5 of BASELINE.json: TP sweep over M for both ops (Llama-3-70B MLP, N=28672,
 # K=8192 hidden): AG ProblemShape(M, 28672/TP, 8192), RS ProblemShape(M, 8192, 28672/TP)

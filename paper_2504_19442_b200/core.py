@@ -892,7 +892,12 @@ class World:
         once they have issued a collective (``.cpu()``, ``.item()``, pageable
         ``.to('cuda')``): the CUDA driver serialises pageable copies, so a rank
         waiting on its stream there can hold back a sibling's launch that its
-        stream is waiting for.  Stage inputs first, return device tensors."""
+        stream is waiting for.  Stage inputs first, return device tensors.
+        For the same reason every CUDA kernel a body launches between
+        collectives (a torch op, say) should have run once before: under lazy
+        module loading its first launch synchronises the context, i.e. waits
+        for a sibling's spinning wait that waits for this rank (the library
+        preloads its own kernels)."""
         if self._closed:
             raise ConfigurationError("world is closed")
         if self._broken:

@@ -1,4 +1,2 @@
-timeout 600 python tp_proxy.py 30 > gpurun_out/proxy.json 2> gpurun_out/proxy.err; echo "proxy rc=$?"; tail -3 gpurun_out/proxy.err
-for m in preset paced; do
-PROXY_MODE=$m timeout 300 python scripts/proxy_trace.py 8 > gpurun_out/trace_$m.json 2> gpurun_out/trace_$m.err; echo "$m rc=$?"; cat gpurun_out/trace_$m.json; tail -2 gpurun_out/trace_$m.err
-done
+timeout 900 python -m pytest tests/test_gpu_litmus.py -q -p no:cacheprovider --durations=3 > gpurun_out/litmus.log 2>&1; echo rc=$?
+grep -E "^E |passed|failed|call" gpurun_out/litmus.log | head -30

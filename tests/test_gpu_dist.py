@@ -68,19 +68,27 @@ def _worker(rank, world, port, q):
         # the default reset=True path, back to back: every join zeroes the
         # flags only after both processes drained (World._quiescent), so no
         # late peer store survives the reset and every call is exact
+        why = [] if ok_rs else ["back-to-back rs mismatch"]
         for it in range(4):
             h, y = world_obj.run(lambda pe: (
                 sb.ag_gemm(pe, x, bb, ag_shape, sb.ag_order_switch(pe.rank, world), agb),
                 sb.gemm_rs(pe, a, bb, rs_shape, sb.rs_inter_order(pe.ctx, 1, world), rsb)))[0]
             ok_ag = ok_ag and np.array_equal(h.float().cpu().numpy(),
                                              oracle.ag_gemm_reference(shards, b))
-            ok_rs = ok_rs and np.array_equal(y.float().cpu().numpy(), ref)
-            ok_rs = ok_rs and world_obj.sweep_signals() == {}
+            yv = y.float().cpu().numpy()
+            if not np.array_equal(yv, ref):
+                why.append(f"it{it}: rs max|diff| {np.abs(yv - ref).max()} at "
+                           f"{np.unravel_index(np.abs(yv - ref).argmax(), ref.shape)}")
+                ok_rs = False
+            hot = world_obj.sweep_signals()
+            if hot:
+                why.append(f"it{it}: hot signals {hot}")
+                ok_rs = False
         gathered = world_obj.read_tensor(rank, agb.gathered, torch.bfloat16, (256 * world, 128))
         ok_layout = np.array_equal(gathered.float().cpu().numpy(), oracle.gathered_layout(shards))
         dist.barrier()
         world_obj.close()
-        q.put((rank, ok_ag, ok_rs, ok_layout, ""))
+        q.put((rank, ok_ag, ok_rs, ok_layout, "; ".join(why) if not ok_rs else ""))
     except Exception as e:  # noqa: BLE001
         q.put((rank, False, False, False, f"{type(e).__name__}: {e}"))
     finally:
