@@ -21,6 +21,7 @@ from pathlib import Path
 
 import numpy as np
 
+from . import schemas
 from .errors import ConfigurationError, ShmemError
 
 EXIT_OK = 0
@@ -31,7 +32,8 @@ _MISMATCH_LIMIT = 20
 _WORLD_KEYS = {"world_size", "n_nodes", "local_world_size", "heap_bytes", "signal_count",
                "timeout_s"}
 _PROBLEM_KEYS = {"m", "n", "k", "dtype", "tile_m", "tile_n", "bytes_per_rank", "elems_per_rank"}
-_TOP_KEYS = {"scenario", "world", "problem", "trials", "iterations", "axes", "measure"}
+_TOP_KEYS = {"scenario", "world", "problem", "trials", "iterations", "axes", "measure", "params",
+             "allocations", "sm_total", "inject_corrupt"}
 
 _DESCRIPTIONS = {
     "allgather-push": "push-mode AllGather on the GPU heap vs byte concatenation",
@@ -46,6 +48,7 @@ _DESCRIPTIONS = {
 def _validate_scenario(doc, what):
     if not isinstance(doc, dict) or "scenario" not in doc:
         raise ConfigurationError(f"{what}: a scenario object with a 'scenario' key is required")
+    schemas.validate(doc, "scenario", what)
     extra = set(doc) - _TOP_KEYS
     if extra:
         raise ConfigurationError(f"{what}: unknown keys {sorted(extra)}")
@@ -262,7 +265,10 @@ def _load(args):
     return doc
 
 
-def _emit(out_dir, filename, doc):
+def _emit(out_dir, filename, doc, schema_name):
+    """Validate ``doc`` against its contract (reference cli.py:78-85), then
+    write it (when an output directory was given)."""
+    schemas.validate(doc, schema_name, filename)
     if out_dir is None:
         return None
     out_dir.mkdir(parents=True, exist_ok=True)
@@ -281,7 +287,7 @@ def cmd_verify(args):
     mismatches = runner(doc, args)
     summary = {"scenario": name, "kind": "verify", "ok": not mismatches, "seed": args.seed or 0,
                "scheduler": "free", "trials": doc.get("trials", 3), "mismatches": mismatches}
-    path = _emit(Path(args.out) if args.out else None, f"{name}_summary.json", summary)
+    path = _emit(Path(args.out) if args.out else None, f"{name}_summary.json", summary, "summary")
     print(json.dumps(summary if not path else {**summary, "written": path}, indent=2))
     return EXIT_OK if not mismatches else EXIT_FAIL
 
@@ -293,13 +299,13 @@ def cmd_tune(args):
         raise ConfigurationError(f"unknown tune scenario {name!r}; choices: ['ag-gemm-tile']")
     report = _tune_ag_gemm_tile(doc, args)
     out_dir = Path(args.out) if args.out else None
-    path = _emit(out_dir, f"{name}_report.json", json.loads(report.to_json()))
+    path = _emit(out_dir, f"{name}_report.json", json.loads(report.to_json()), "tune_report")
     summary = {"scenario": name, "kind": "tune", "ok": True, "seed": args.seed or 0,
                "scheduler": "free", "chosen_index": report.chosen_index,
                "chosen_config": report.chosen_config, "scores_us": report.scores}
     if path:
         summary["outputs"] = {"report": path}
-    _emit(out_dir, f"{name}_summary.json", summary)
+    _emit(out_dir, f"{name}_summary.json", summary, "summary")
     print(json.dumps(summary, indent=2))
     return EXIT_OK
 

@@ -84,18 +84,19 @@ def read_trace(world, rank, records_per_cta, launches):
 
 
 def to_chrome_trace(events):
-    """Chrome trace (chrome://tracing / Perfetto): pid = rank, tid = CTA."""
+    """Chrome trace event list (chrome://tracing / Perfetto), the reference's
+    shape (costmodel.py:185-190, schemas.TRACE): pid = rank, tid = the CTA
+    as a resource name, times in us from the earliest record."""
     if not events:
-        return {"traceEvents": []}
+        return []
     base = min(e["t0_ns"] for e in events)
     out = []
     for e in events:
         name = e["op"] if e["chunk"] is None else f"{e['op']}[c{e['chunk']}]"
         out.append({"name": f"{e['kernel']}#{e['launch']} {name}", "ph": "X",
                     "ts": (e["t0_ns"] - base) / 1e3, "dur": (e["t1_ns"] - e["t0_ns"]) / 1e3,
-                    "pid": e["rank"], "tid": e["cta"],
-                    "args": {"tile": e["tile"], "chunk": e["chunk"]}})
-    return {"traceEvents": out, "displayTimeUnit": "ns"}
+                    "pid": e["rank"], "tid": f"cta{e['cta']}"})
+    return out
 
 
 def exposed_comm(events):

@@ -34,3 +34,31 @@ def test_unknown_keys_and_scenarios_are_usage_errors(tmp_path):
     assert cli.main(["verify", "--config", str(p)]) == cli.EXIT_USAGE
     p.write_text(json.dumps({"scenario": "ag-gemm"}))
     assert cli.main(["tune", "--config", str(p)]) == cli.EXIT_USAGE
+
+
+def test_emitted_documents_are_schema_checked(tmp_path):
+    """Every file the CLI writes is validated against its contract first
+    (reference cli.py:78-85): a conforming summary is written, a broken one
+    is a usage error naming the document."""
+    import pytest
+
+    from paper_2504_19442_b200 import schemas
+    from paper_2504_19442_b200.errors import ConfigurationError
+
+    ok = {"scenario": "ag-gemm", "kind": "verify", "ok": True, "mismatches": []}
+    path = cli._emit(tmp_path, "s_summary.json", ok, "summary")
+    assert json.loads(open(path).read()) == ok
+    with pytest.raises(ConfigurationError, match="summary schema"):
+        cli._emit(tmp_path, "bad_summary.json", {"scenario": "x", "kind": "bogus", "ok": 1},
+                  "summary")
+    report = {"axes": {"bn": [128, 256]}, "configs": [{"bn": 128}, {"bn": 256}],
+              "timings_us": [[[1.0, 2.0]], None], "scores": [1.5, None], "chosen_index": 0,
+              "chosen_config": {"bn": 128}, "per_rank_chosen": [0], "invalid": {"1": "bad"}}
+    schemas.validate(report, "tune_report", "r")
+    with pytest.raises(ConfigurationError):
+        schemas.validate({**report, "extra": 1}, "tune_report", "r")
+    with pytest.raises(ConfigurationError):
+        schemas.validate({"scenario": "ag-gemm", "trials": 0}, "scenario", "s")
+    schemas.validate({"scenario": "ag-gemm", "world": {"world_size": 2},
+                      "problem": {"m": 8, "n": 8, "k": 8, "dtype": "bfloat16"}, "trials": 2},
+                     "scenario", "s")

@@ -3,6 +3,7 @@ summary (the device side is covered by test_gpu_timeline.py)."""
 
 import json
 
+from paper_2504_19442_b200 import schemas
 from paper_2504_19442_b200.timeline import exposed_comm, to_chrome_trace
 
 
@@ -14,14 +15,14 @@ def ev(op, cta, t0, t1, rank=0, launch=0, kernel="ag_gemm", chunk=None):
 def test_chrome_trace_shape_matches_reference_timeline():
     events = [ev("cta", 0, 1000, 9000), ev("chunk_wait", 0, 2000, 2500, chunk=3),
               ev("tile_epilogue", 1, 4000, 4400, chunk=0)]
-    doc = to_chrome_trace(events)
-    json.dumps(doc)
-    evs = doc["traceEvents"]
+    evs = to_chrome_trace(events)
+    json.dumps(evs)
+    schemas.validate(evs, "trace", "trace")  # the reference's trace contract
     assert {e["ph"] for e in evs} == {"X"}
-    assert {"name", "ts", "dur", "pid", "tid"} <= set(evs[0])
+    assert {"name", "ph", "ts", "dur", "pid", "tid"} == set(evs[0])
     wait = next(e for e in evs if "chunk_wait" in e["name"])
-    assert wait["ts"] == 1.0 and wait["dur"] == 0.5 and wait["tid"] == 0 and "[c3]" in wait["name"]
-    assert to_chrome_trace([]) == {"traceEvents": []}
+    assert wait["ts"] == 1.0 and wait["dur"] == 0.5 and wait["tid"] == "cta0" and "[c3]" in wait["name"]
+    assert to_chrome_trace([]) == []
 
 
 def test_exposed_comm_per_launch():
