@@ -203,8 +203,8 @@ int sh_gemm_workspace_bytes(int m, int n, int k, size_t* bytes);
 int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtype, void* workspace,
             size_t workspace_bytes, void* stream);
 
-/* Tile override for tuning: bn in {0 (auto), 128, 224, 256}; cta_group in {0 (auto), 1, 2}
- * (224 needs cta_group 2). */
+/* Tile override for tuning: bn in {0 (auto), 128, 224, 256, 512}; cta_group in {0 (auto),
+ * 1, 2} (224 and 512 need cta_group 2; 512 = the single-buffered 256x512 pair tile). */
 int sh_set_tile_config(int bn, int cta_group);
 /* Tile-order override for tuning: stream_k -2 unset (env SHB_SK, else auto),
  * -1 auto (split the last waves when they would leave CTA pairs idle), 0 off,

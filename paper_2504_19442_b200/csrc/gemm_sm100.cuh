@@ -311,7 +311,14 @@ struct GemmCfg {
   static constexpr int EPI_NBUF = 4;                 // staging buffers per epilogue warp
   static constexpr int EPI_BYTES = 4 * EPI_NBUF * EPI_BUF;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
-  static_assert(BNC % 16 == 0 && BN % SUB == 0 && BN <= 256, "BN");
+  // BN = 512 (pair tiles only): two N = 256 MMAs per K step into one
+  // accumulator of all 512 TMEM columns -- no second buffer, so the epilogue
+  // is not overlapped with the next tile; chosen only for long-K grids of
+  // about one tile per cluster (e.g. C5 RS at M=1024), where the wide tile
+  // halves the B re-reads and the single epilogue is noise
+  static constexpr int UMMA_N = BN > 256 ? 256 : BN;
+  static constexpr int NACC = 2 * BN <= 512 ? 2 : 1;  // TMEM accumulator buffers
+  static_assert(BNC % 16 == 0 && BN % SUB == 0 && (BN <= 256 || (BN == 512 && CG == 2)), "BN");
   static_assert(CG == 2 || BN % 64 == 0, "1-CTA tiles stage whole 64-column boxes");
   // 227 KB of dynamic smem per CTA, minus alignment slack and barriers
   static constexpr int stages_for_smem() {
@@ -345,9 +352,11 @@ template <int BN, bool FP16>
 __device__ __forceinline__ void reduce_rows(const TileParams& p, int row0, int n0, uint32_t lane) {
   constexpr int kRedRows = 4;
   constexpr int kGroup = 8;
-  const int col = n0 + (int)lane * 8;
-  if ((int)lane * 8 >= BN || col + 8 > p.n) return;
   const size_t slot_elems = (size_t)p.rows * p.n;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 256) {
+  const int col = n0 + c0 + (int)lane * 8;
+  if (c0 + (int)lane * 8 >= BN || col + 8 > p.n) continue;
 #pragma unroll 1
   for (int r0 = 0; r0 < 32; r0 += kRedRows) {
     float acc[kRedRows][8];
@@ -392,6 +401,7 @@ __device__ __forceinline__ void reduce_rows(const TileParams& p, int row0, int n
             make_uint4(pack2(acc[r][0], acc[r][1], FP16), pack2(acc[r][2], acc[r][3], FP16),
                        pack2(acc[r][4], acc[r][5], FP16), pack2(acc[r][6], acc[r][7], FP16));
     }
+  }
   }
 }
 
@@ -499,6 +509,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool copying = own && p.copy_own;
         const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
         const int col0 = nb * BN + (int)cta_rank * BNC;
+        // global column of this CTA's B box j: for BN <= 256 the CTA holds
+        // the contiguous half [col0, col0 + BNC); for BN = 512 it holds the
+        // half of each N = 256 MMA (boxes 0-1 and 2-3 = its 128 columns of
+        // the tile's first and second 256)
+        auto bcol = [&](int j) {
+          return BN > 256 ? nb * BN + (j >> 1) * 256 + (int)cta_rank * 128 + (j & 1) * 64
+                          : col0 + j * 64;
+        };
         if (MODE == MODE_AG && !own) {
           // wait(ready[chunk]) of pipelines.py:130-141, as an acquire spin on
           // the range holding this CTA's last row of the tile
@@ -555,10 +573,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int j = 0; j < C::B_BOXES; ++j) {
                 if constexpr (CG == 1)
-                  tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                  tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, bcol(j), kx,
                               b_hint);
                 else
-                  tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64,
+                  tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, bcol(j),
                                    kx, b_hint);
               }
             } else if constexpr (CG == 1) {
@@ -566,14 +584,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               else tma_load_3d(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, a_hint);
 #pragma unroll
               for (int j = 0; j < C::B_BOXES; ++j)
-                tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                tma_load_2d(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, bcol(j), kx,
                             b_hint);
             } else {
               if (own) tma_load_2d_pair(&maps.a_own, &full[stage], a_dst, kx, row0, a_hint);
               else tma_load_3d_pair(&maps.a_all, &full[stage], a_dst, kx, row0, chunk, a_hint);
 #pragma unroll
               for (int j = 0; j < C::B_BOXES; ++j)
-                tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, col0 + j * 64, kx,
+                tma_load_2d_pair(&maps.b, &full[stage], b_dst + j * 64 * BK * 2, bcol(j), kx,
                                  b_hint);
             }
           }
@@ -593,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     //   A (K-major SW128): +32 B per 16-element K step -> +2 in addr>>4
     //   B (MN-major SW128): +2 KB per 16-row K step   -> +128 in addr>>4
     if (leader) {
-      constexpr uint32_t IDESC = umma_idesc_f16(BM * CG, BN, FP16 ? 0 : 1, /*a K-major*/ 0,
+      constexpr uint32_t IDESC = umma_idesc_f16(BM * CG, C::UMMA_N, FP16 ? 0 : 1, /*a K-major*/ 0,
                                                 /*b MN-major*/ 1);
       const uint64_t a_desc0 = umma_desc(smem_u32(sA), 16, 1024, 2);
       // B: 64-column atoms 8 KB apart (LBO), 8-row K groups 1 KB apart (SBO)
@@ -609,8 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       wi.init(p, cluster_id, num_clusters, num_kb, ring, 1, CG);
       WorkItem w;
       for (; wi.next(w); ++it) {
-        const int as = it & 1;
-        const uint32_t aphase = (it >> 1) & 1;
+        const int as = C::NACC == 2 ? (it & 1) : 0;
+        const uint32_t aphase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
         const uint64_t tw0 = mtrace ? globaltimer() : 0;
         mbar_wait_cluster(&tempty[as], aphase ^ 1);
         const uint64_t tw1 = mtrace ? globaltimer() : 0;
@@ -632,8 +650,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bd = b_desc0 + (uint64_t)((stage * C::B_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
+            for (int kk = 0; kk < BK / 16; ++kk) {
               umma_f16<CG>(d_tmem, ad + 2 * kk, bd + 128 * kk, IDESC, (i != 0) || (kk != 0));
+              if constexpr (BN > 256)  // second 256 columns: B boxes 2-3 (16 KB on)
+                umma_f16<CG>(d_tmem + 256, ad + 2 * kk, bd + 1024 + 128 * kk, IDESC,
+                             (i != 0) || (kk != 0));
+            }
             umma_commit<CG>(&empty[stage]);
           }
           __syncwarp();
@@ -714,8 +736,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (; wi.next(w); ++it) {
       int chunk, mb, nb;
       decode_tile(p, w.t, chunk, mb, nb);
-      const int as = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
+      const int as = C::NACC == 2 ? (it & 1) : 0;
+      const uint32_t aphase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
       const int cta_row0 = mb * (BM * CG) + (int)cta_rank * BM;
       const int row = cta_row0 + q * 32;  // first row of this warp's slab
       const int n0 = nb * BN;

@@ -133,6 +133,9 @@ int stream_k_split(const Cfg& c, int num_kb) {
     mode = env ? (atoi(env) != 0 ? 1 : 0) : -1;
   }
   if (mode == 0) return c.tiles;
+  // wide tiles: one wave by construction, and splitting K would put the
+  // m-blocks of a column block at different k (B re-read from DRAM)
+  if (c.bn == 512 && mode != 1) return c.tiles;
   const int waves = (c.tiles + clusters - 1) / clusters;
   const double eff = double(c.tiles) / double(waves * clusters);
   const bool want = mode == 1 || (eff < 0.92 && num_kb >= 8);
@@ -242,10 +245,24 @@ int raster_group(int rows, int k, int mblk, int bm, int clusters) {
   return (mblk + ngroups - 1) / ngroups;
 }
 
-Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1) {
+Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1, int k = 0) {
   // ranks sharing one GPU split its SMs, so that all their persistent GEMMs
   // are co-resident (their epilogues wait on each other's stores)
   if (share > 1) sms = std::max(2, (sms / share) & ~1);
+  // Wide 256 x 512 pair tiles for long-K grids of at most one tile per
+  // cluster: every cluster then streams its own 512 B columns once, all
+  // m-blocks of a column block walk K together (B leaves DRAM once), and the
+  // single-buffered accumulator's epilogue happens once.  C5 RS at M=1024
+  // (k=28672): 256x256 stream-K read 1.85 GB from DRAM for a 0.53 GB
+  // problem (ncu, profiles/README.md); cuBLAS picks 256x512 there too.
+  if (g_force_bn == 512 ||
+      (!g_force_bn && k >= 8192 && rows > 128 && g_force_cg != 1 && n % 512 == 0)) {
+    const int mblk = (rows + 255) / 256, nblk = (n + 511) / 512, tiles = world * mblk * nblk;
+    if (g_force_bn == 512 || (tiles <= sms / 2 && tiles * 2 > sms / 2)) {
+      const int clusters = std::min(tiles, sms / 2);
+      return Cfg{512, 2, clusters * 2, mblk, nblk, tiles};
+    }
+  }
   int cgs[2] = {2, 1};
   int bns[3] = {256, 224, 128};
   Cfg best{};
@@ -400,6 +417,7 @@ template <int MODE, bool FP16>
 int launch_mode(const Cfg& c, const TensorMaps& maps, const TileParams& p, cudaStream_t s,
                 bool pdl) {
   if (c.cg == 2) {
+    if (c.bn == 512) return launch_one<512, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
     if (c.bn == 256) return launch_one<256, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
     if (c.bn == 224) return launch_one<224, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
     return launch_one<128, 2, MODE, FP16>(maps, p, c.grid, s, pdl);
@@ -469,6 +487,7 @@ cudaError_t preload_one() {
 template <int MODE, bool FP16>
 cudaError_t preload_mode() {
   cudaError_t e;
+  if ((e = preload_one<512, 2, MODE, FP16>())) return e;
   if ((e = preload_one<256, 2, MODE, FP16>())) return e;
   if ((e = preload_one<224, 2, MODE, FP16>())) return e;
   if ((e = preload_one<128, 2, MODE, FP16>())) return e;
@@ -651,7 +670,9 @@ int init_rank_common(sh_world* w, RankState& rs) {
   int rc = ensure_preloaded(rs.device);
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(rs.device));
-  if ((rc = sk_reserve(rs.sk, num_sms(rs.device) / 2, 2, 256))) return rc;
+  // sized for the widest tile up front: a later growth would synchronise
+  // the device, i.e. wait for a sibling rank's spinning GEMM
+  if ((rc = sk_reserve(rs.sk, num_sms(rs.device) / 2, 2, 512))) return rc;
   CUDA_TRY(cudaMalloc(&rs.tile_counter, 256));
   CUDA_TRY(cudaMemset(rs.tile_counter, 0, 256));
   CUDA_TRY(cudaMalloc(&rs.wave, kWaveFlags * sizeof(uint64_t)));
@@ -1016,8 +1037,9 @@ int sh_clear_error(sh_world* w, int rank) {
 }
 
 int sh_set_tile_config(int bn, int cta_group) {
-  if (bn != 0 && bn != 128 && bn != 224 && bn != 256)
-    return fail(SH_ERR_ARG, "bn must be 0, 128, 224 or 256");
+  if (bn != 0 && bn != 128 && bn != 224 && bn != 256 && bn != 512)
+    return fail(SH_ERR_ARG, "bn must be 0, 128, 224, 256 or 512");
+  if (bn == 512 && cta_group == 1) return fail(SH_ERR_ARG, "bn 512 needs cta_group 2");
   if (cta_group < 0 || cta_group > 2) return fail(SH_ERR_ARG, "cta_group must be 0, 1 or 2");
   g_force_bn = bn;
   g_force_cg = cta_group;
@@ -1181,7 +1203,7 @@ int sh_gemm_workspace_bytes(int m, int n, int k, size_t* bytes) {
   if (m < 1 || n < 1 || k < 1) return fail(SH_ERR_ARG, "m, n, k must be >= 1");
   int dev = 0;
   cudaGetDevice(&dev);
-  Cfg cfg = choose_cfg(m, 1, n, num_sms(dev));
+  Cfg cfg = choose_cfg(m, 1, n, num_sms(dev), 1, k);
   *bytes = kCounterBytes +
            (stream_k_split(cfg, (k + 63) / 64) < cfg.tiles ? sk_workspace_bytes(cfg) : 0);
   return SH_OK;
@@ -1198,7 +1220,7 @@ int sh_gemm(const void* a, const void* b, void* c, int m, int n, int k, int dtyp
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   if ((rc = ensure_preloaded(dev))) return rc;
-  Cfg cfg = choose_cfg(m, 1, n, num_sms(dev));
+  Cfg cfg = choose_cfg(m, 1, n, num_sms(dev), 1, k);
   TensorMaps maps;
   memset(&maps, 0, sizeof(maps));
   const uint64_t es = 2;
@@ -1325,7 +1347,7 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = rs->device;
-  Cfg cfg = choose_cfg(rows, W, n, num_sms(dev), rs->ranks_on_device);
+  Cfg cfg = choose_cfg(rows, W, n, num_sms(dev), rs->ranks_on_device, k);
   const bool own_by_ce = env_int("SHB_OWN_COPY_CE", 0) != 0;
   const bool do_comm = phase != SH_PHASE_COMPUTE;
   const bool do_compute = phase != SH_PHASE_COMM;
@@ -1507,7 +1529,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   }
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device), rs->ranks_on_device);
+  Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device), rs->ranks_on_device, k);
   const bool fuse = rs_fused(rs_phase);
   // With the reduction fused, the tiles of my own chunk wait for every peer's
   // rows; a cluster that reached them before finishing its peer-chunk tiles

@@ -22,9 +22,9 @@ def _default_cfg():
     _lib.check(_lib.load().sh_set_tile_config(0, 0))
 
 
-@pytest.mark.parametrize("bn,cg", [(256, 2), (224, 2), (128, 2), (256, 1), (128, 1)])
+@pytest.mark.parametrize("bn,cg", [(512, 2), (256, 2), (224, 2), (128, 2), (256, 1), (128, 1)])
 @pytest.mark.parametrize("m,n,k", [(256, 256, 64), (512, 512, 512), (1024, 768, 1024),
-                                   (384, 320, 200), (1000, 520, 136)])
+                                   (384, 320, 200), (1000, 520, 136), (1024, 1536, 8448)])
 def test_gemm_matches_fp32(bn, cg, m, n, k):
     _lib.check(_lib.load().sh_set_tile_config(bn, cg))
     g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
