@@ -11,6 +11,7 @@ torch = pytest.importorskip("torch")
 from paper_2504_19442_b200 import (ProblemShape, WorldSpec, ag_gemm, ag_order_switch,  # noqa: E402
                                    gemm_rs, init_world, make_ag_gemm_buffers,
                                    make_gemm_rs_buffers, rs_inter_order)
+from paper_2504_19442_b200 import schemas  # noqa: E402
 from paper_2504_19442_b200.timeline import exposed_comm, to_chrome_trace  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -45,6 +46,7 @@ def test_trace_of_a_tp_mlp_step(tmp_path):
             assert e["t1_ns"] >= e["t0_ns"] > 0
     doc = to_chrome_trace(events)
     json.dumps(doc)
-    assert doc["traceEvents"] and all(ev["ph"] == "X" for ev in doc["traceEvents"])
+    assert doc and all(ev["ph"] == "X" for ev in doc)
+    schemas.validate(doc, "trace", "trace")  # the reference's trace contract
     summary = exposed_comm(events)
     assert len(summary) == 2 * W and all(s["span_us"] > 0 for s in summary)
