@@ -740,7 +740,8 @@ class World:
         code = self.poll_error(rank)
         if code:
             what = {1: "AllGather chunk flag", 2: "ReduceScatter slot release",
-                    3: "ReduceScatter arrival counter", 4: "stream flag wait"}.get(code, "flag")
+                    3: "ReduceScatter arrival counter", 4: "stream flag wait",
+                    5: "stream-K partial", 6: "own-chunk staging stores"}.get(code, "flag")
             raise SynchronizationFault(
                 f"rank {rank}: device wait on {what} exceeded {self.spec.timeout_s} s")
 

@@ -39,7 +39,9 @@ struct TileParams {
   int mblk, nblk;  // m-blocks per chunk, n-blocks
   int num_tiles;   // world * mblk * nblk
   int group_m;     // raster group (m-blocks) for L2 reuse
-  int serpentine;  // odd raster groups walk n backwards
+  int merge;       // leading chunk positions rastered as one region (<= 1: none)
+  int group_m_merged;  // raster group of that region
+  int serpentine;  // odd raster groups walk n backwards (2: parity continues across chunks)
   int kserp;       // every other data-parallel tile of a cluster walks K backwards
   int order[kMaxWorld];  // chunk visit order (reference swizzle.py)
   uint64_t epoch;
@@ -52,6 +54,7 @@ struct TileParams {
   uint64_t rs_target;                 // RS: epoch * rows * n, a chunk fully delivered
   const uint16_t* staging_local;      // RS: my staging buffer (W slots of rows x n)
   int fuse_reduce;                    // RS: reduce my chunk in the epilogue of its tiles
+  int red_help;                       // RS fused: idle warps share the own-chunk reduction
   uint16_t* out_rows;                 // RS: the reduced output rows (rows x n, row-major)
   int copy_own;                       // AG: store own-chunk A stages into gathered[rank]
   // optional timeline: per CTA `trace_cap` records of 4 u64 {kind|aux, t0, t1, tile}
@@ -64,7 +67,8 @@ struct TileParams {
   int trace_cap;
   uint64_t l2_hint_a, l2_hint_b;      // TMA L2 cache policies of the operand loads
   uint64_t l2_hint_store;             // RS: L2 policy of the staging / output stores
-  uint64_t l2_hint_own;               // AG: L2 policy of the own-slot stores
+  uint64_t l2_hint_own;               // AG: L2 policy of the own-slot stores; RS: of the
+                                      // own chunk's staging stores (fused, W > 1)
   // stream-K tail: tiles [0, dp_tiles) are data-parallel (one cluster each);
   // the k-blocks of tiles [dp_tiles, num_tiles) are split evenly over all
   // clusters.  A cluster's range is walked backwards, so the partial head of a
@@ -277,23 +281,47 @@ struct TensorMaps {
   CUtensorMap own_slot;        // AG: my gather slot `rank`, {k, rows} (box = one A stage)
 };
 
+// Tile t -> (chunk, m-block, n-block).  Tiles are enumerated position by
+// position of the chunk order; the first `merge` positions (RS: every peer
+// chunk, the own chunk staying last) may form ONE raster region whose
+// m-blocks are those of all its chunks, so a raster group spans several
+// chunks and B is streamed once per group instead of once per chunk.
 __device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chunk, int& mb,
                                             int& nb) {
   const int per_chunk = p.mblk * p.nblk;
-  const int s = t / per_chunk;
-  const int w = t - s * per_chunk;
-  chunk = p.order[s];
-  const int gm = p.group_m;
+  const int merged = p.merge > 1 ? p.merge : 0;
+  int w, vblk, gm, s0, g0;  // index in region, its m-blocks, raster group, first position, groups before
+  if (t < merged * per_chunk) {
+    w = t;
+    vblk = merged * p.mblk;
+    gm = p.group_m_merged;
+    s0 = 0;
+    g0 = 0;
+  } else {
+    const int s = merged + (t - merged * per_chunk) / per_chunk;
+    w = t - s * per_chunk;
+    vblk = p.mblk;
+    gm = p.group_m;
+    s0 = s;
+    const int gpre = merged ? (merged * p.mblk + p.group_m_merged - 1) / p.group_m_merged : 0;
+    g0 = gpre + (s - merged) * ((p.mblk + gm - 1) / gm);
+  }
   const int span = gm * p.nblk;
   const int group = w / span;
   const int first_m = group * gm;
-  const int gsize = min(p.mblk - first_m, gm);
+  const int gsize = min(vblk - first_m, gm);
   const int in = w - group * span;
-  mb = first_m + in % gsize;
+  const int vm = first_m + in % gsize;
   nb = in / gsize;
+  const int vs = vm / p.mblk;  // chunk position inside a merged region (0 otherwise)
+  chunk = p.order[s0 + vs];
+  mb = vm - vs * p.mblk;
   // serpentine: odd groups walk the n-blocks backwards, so a group starts on
-  // the B columns its predecessor finished with (still in L2)
-  if (p.serpentine && (group & 1)) nb = p.nblk - 1 - nb;
+  // the B columns its predecessor finished with (still in L2).  2: the parity
+  // runs on across chunks / regions, so the next chunk opens on the columns
+  // the previous one touched last instead of the ones it touched first
+  const int gidx = p.serpentine == 2 ? g0 + group : group;
+  if (p.serpentine && (gidx & 1)) nb = p.nblk - 1 - nb;
 }
 
 template <int BN, int CG>
@@ -348,17 +376,18 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi, bool fp16) {
 // contiguous bytes of one source's row; kRedRows rows x up to 8 sources are
 // in flight per lane before the first add.  Sum in ascending source order
 // from +0.0f in fp32, rounded once (reference collectives.py:163-171).
-template <int BN, bool FP16>
+template <int BN, bool FP16, int NROWS = 32>
 __device__ __forceinline__ void reduce_rows(const TileParams& p, int row0, int n0, uint32_t lane) {
   constexpr int kRedRows = 4;
   constexpr int kGroup = 8;
+  static_assert(NROWS % kRedRows == 0, "rows per call");
   const size_t slot_elems = (size_t)p.rows * p.n;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 256) {
   const int col = n0 + c0 + (int)lane * 8;
   if (c0 + (int)lane * 8 >= BN || col + 8 > p.n) continue;
 #pragma unroll 1
-  for (int r0 = 0; r0 < 32; r0 += kRedRows) {
+  for (int r0 = 0; r0 < NROWS; r0 += kRedRows) {
     float acc[kRedRows][8];
 #pragma unroll
     for (int r = 0; r < kRedRows; ++r)
@@ -405,6 +434,65 @@ __device__ __forceinline__ void reduce_rows(const TileParams& p, int row0, int n
   }
 }
 
+// Cooperative own-chunk reduction (MODE_RS, fused, W > 1).  The 128 rows a
+// CTA holds of an own-chunk tile are reduced in kRedUnits units of 8 rows,
+// numbered globally (unit g belongs to the CTA's (g / kRedUnits)-th own tile).
+// The four epilogue warps store their rows into staging[rank], bump
+// `stored`, and claim units of that tile; warps with nothing else to do --
+// the copier warp (idle in RS), the non-leader CTA's MMA warp, and the
+// producer / MMA warps once their loops end -- walk the same own tiles and
+// claim units too.  At the tail of the launch (the last own tile, which no
+// MMA overlaps) six or seven warps share the reduction instead of four.
+// Counters are monotone smem words: ctr[0] units claimed, ctr[1] epilogue
+// warps that finished storing (tile o stored <=> ctr[1] >= 4 (o + 1)).
+constexpr int kRedUnits = 16;
+
+// lane 0: claim the next unit of own tile o, -1 when all of its units are taken
+__device__ __forceinline__ int claim_unit(uint32_t* next, int o) {
+  const uint32_t limit = (uint32_t)(o + 1) * kRedUnits;
+  uint32_t cur = *reinterpret_cast<volatile uint32_t*>(next);
+  while (cur < limit) {
+    const uint32_t prev = atomicCAS(next, cur, cur + 1);
+    if (prev == cur) return (int)(cur - (uint32_t)o * kRedUnits);
+    cur = prev;
+  }
+  return -1;
+}
+
+// warp-wide: reduce every unit of own tile o this warp can claim
+template <int BN, int CG, bool FP16>
+__device__ __forceinline__ void reduce_own_units(const TileParams& p, uint32_t* ctr, int o, int mb,
+                                                 int nb, uint32_t cta_rank, uint32_t lane) {
+  for (;;) {
+    int u = 0;
+    if (lane == 0) {
+      u = claim_unit(&ctr[0], o);
+      if (u >= 0) {
+        // every epilogue warp's rows of tile o are in staging[rank]
+        // (the epilogue warps always get there, also after a failed peer
+        // wait; bounded all the same, like every other spin)
+        const uint32_t want = 4u * (uint32_t)(o + 1);
+        uint64_t t0 = 0;
+        while (*reinterpret_cast<volatile uint32_t*>(&ctr[1]) < want) {
+          __nanosleep(128);
+          const uint64_t now = globaltimer();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > p.timeout_ns) {
+            if (p.err) atomicCAS(p.err, 0, 6);
+            u = -1;
+            break;
+          }
+        }
+        __threadfence_block();
+      }
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u < 0) return;
+    reduce_rows<BN, FP16, 128 / kRedUnits>(p, mb * (128 * CG) + (int)cta_rank * 128 + u * 8,
+                                           nb * BN, lane);
+  }
+}
+
 constexpr int kThreads = 224;  // 7 warps: producer, MMA, 4 epilogue, own-slot copier
 
 template <int BN, int CG, int MODE, bool FP16>
@@ -427,6 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* alanded_bar = stored_bar + STAGES;  // AG own copy: this CTA's A half landed
   TileRing* ring = reinterpret_cast<TileRing*>(alanded_bar + STAGES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 1);
+  uint32_t* red_ctr = tmem_slot + 1;  // cooperative own-chunk reduction (2 words)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -462,6 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ring->full[r], 1);
       mbar_init(&ring->empty[r], per_cta * CG);
     }
+    red_ctr[0] = 0;
+    red_ctr[1] = 0;
     fence_mbarrier_init();
   }
   if (warp == 2) tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
@@ -726,6 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool peers_in = false;  // RS fused: every peer's contribution to my chunk landed
     int pend_chunk = -1;    // RS: tile whose stores still have to be published
     uint64_t pend_count = 0;
+    int own_o = 0;          // RS fused: own-chunk tiles reduced so far (unit numbering)
     const size_t slot_elems = (size_t)p.rows * p.n;
     const bool tracer = p.trace != nullptr && warp == 2 && lane == 0;
     const uint64_t t_cta0 = tracer ? globaltimer() : 0;
@@ -882,7 +974,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (MODE == MODE_AG) {
               tma_store_3d_hint(&maps.c, sb, xcol, row, chunk, p.l2_hint_store);
             } else {
-              tma_store_2d_hint(&maps.out[chunk], sb, xcol, row, p.l2_hint_store);
+              // own chunk at W > 1: re-read by the reduction right away
+              tma_store_2d_hint(&maps.out[chunk], sb, xcol, row,
+                                fused_own && p.world > 1 ? p.l2_hint_own : p.l2_hint_store);
               if (dual) tma_store_3d_hint(&maps.c, sb, xcol, row, 0, p.l2_hint_store);
             }
             bulk_commit();
@@ -903,10 +997,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           bulk_wait<0>();
           fence_proxy_async_global();
+          __threadfence_block();
+          atomicAdd(&red_ctr[1], 1u);  // this warp's rows of own tile own_o are stored
         }
         __syncwarp();
         const uint64_t tr1 = tracer ? globaltimer() : 0;
-        reduce_rows<BN, FP16>(p, row, n0, lane);
+        // units of this tile, shared with the helper warps (cta_row0 = the
+        // CTA's 128 rows; the units span all four epilogue warps' rows)
+        reduce_own_units<BN, CG, FP16>(p, red_ctr, own_o, mb, nb, cta_rank, lane);
+        ++own_o;
         if (tracer)  // kind 6: own-chunk reduction, aux = store-drain part (ns)
           trace_rec(p, trace_slot++, (6ull << 56) | ((tr1 - tr0) & 0xFFFFFFFFull), tr0, globaltimer(),
                     w.t);
@@ -955,6 +1054,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
 
+  if constexpr (MODE == MODE_RS) {
+    // helper warps of the cooperative own-chunk reduction (see kRedUnits):
+    // the copier warp and the non-leader MMA warp from the start, the
+    // producer and the leader's MMA warp once their loops are done.  They
+    // walk the same static schedule (not with the dynamic tile counter).
+    if ((warp == 0 || warp == 1 || warp == 6) && p.fuse_reduce && p.red_help && p.world > 1 &&
+        p.tile_counter == nullptr) {
+      WorkIter wi;
+      wi.init(p, cluster_id, num_clusters, num_kb);
+      WorkItem w;
+      int o = 0;
+      while (wi.next(w)) {
+        int chunk, mb, nb;
+        decode_tile(p, w.t, chunk, mb, nb);
+        if (chunk != p.rank || w.kind == 1) continue;  // kind 1: partial head, no epilogue
+        reduce_own_units<BN, CG, FP16>(p, red_ctr, o, mb, nb, cta_rank, lane);
+        ++o;
+      }
+    }
+  }
+
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 2) {
@@ -968,52 +1088,52 @@ __global__ void __launch_bounds__(kThreads, 1)
 // as bf16/fp16 (reference collectives.py:163-171; fixed ascending source
 // order keeps the float result reproducible).  Each CTA waits
 // for every source's element counter to reach epoch*rows*n first.
+// HBM-bound: (W + 1) * rows * n * 2 bytes.  Every source's 16-byte vector of
+// an element group is loaded before the first add (8 loads in flight per
+// thread): the per-source load -> add loop ran at 4.3 TB/s on the C4/TP=8
+// layout (ncu, 31.4 us), this form at ~7 TB/s (scripts/probe/reduce_bw.cu:
+// 20.8 us; the slot stride -- exactly 16 MB there -- makes no difference).
 template <bool FP16>
 __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restrict__ staging,
                                                         uint16_t* __restrict__ out,
                                                         size_t slot_elems, int world,
                                                         const uint64_t* counters, uint64_t target,
                                                         int* err, uint64_t timeout_ns) {
+  constexpr int kGroup = 8;
   if (threadIdx.x == 0) {
     for (int s = 0; s < world; ++s) spin_geq(counters + s, target, err, timeout_ns, 3);
   }
   __syncthreads();
-  const size_t nvec = slot_elems / 8;
+  // 16-byte vectors only when every slot starts 16-byte aligned
+  const size_t nvec = (slot_elems % 8 == 0) ? slot_elems / 8 : 0;
   const uint4* st = reinterpret_cast<const uint4*>(staging);
   uint4* o = reinterpret_cast<uint4*>(out);
-  const size_t slot_vec = slot_elems / 8;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nvec;
        i += (size_t)gridDim.x * blockDim.x) {
     float acc[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-    for (int s = 0; s < world; ++s) {
-      uint4 v = __ldcs(st + s * slot_vec + i);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (int s0 = 0; s0 < world; s0 += kGroup) {
+      uint4 v[kGroup];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float lo, hi;
-        if (FP16) {
-          __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
-          float2 f = __half22float2(h);
-          lo = f.x; hi = f.y;
-        } else {
-          __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
-          float2 f = __bfloat1622float2(h);
-          lo = f.x; hi = f.y;
+      for (int g = 0; g < kGroup; ++g)
+        v[g] = s0 + g < world ? __ldcs(st + (size_t)(s0 + g) * nvec + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) {
+        if (s0 + g >= world) break;
+        const uint32_t w[4] = {v[g].x, v[g].y, v[g].z, v[g].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = unpack2(w[e], FP16);
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
         }
-        acc[2 * e] += lo;
-        acc[2 * e + 1] += hi;
       }
     }
-    uint4 r;
-    r.x = pack2(acc[0], acc[1], FP16);
-    r.y = pack2(acc[2], acc[3], FP16);
-    r.z = pack2(acc[4], acc[5], FP16);
-    r.w = pack2(acc[6], acc[7], FP16);
-    __stcs(o + i, r);
+    __stcs(o + i, make_uint4(pack2(acc[0], acc[1], FP16), pack2(acc[2], acc[3], FP16),
+                             pack2(acc[4], acc[5], FP16), pack2(acc[6], acc[7], FP16)));
   }
-  // scalar tail (slot_elems % 8)
+  // scalar remainder (every element when the slots are not 16-byte aligned)
   const size_t tail0 = nvec * 8;
   for (size_t i = tail0 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < slot_elems;
        i += (size_t)gridDim.x * blockDim.x) {

@@ -453,8 +453,12 @@ int launch_gemm(int dtype, const Cfg& c, const TensorMaps& maps, const TileParam
   // reuses (C4: DRAM reads 259 -> 229 MB per launch)
   p.l2_hint_store = MODE == MODE_RS ? l2_policy("SHB_HINT_STORE", kEvictFirst)
                                      : l2_policy("SHB_HINT_STORE_AG", kEvictNormal);
-  p.l2_hint_own = l2_policy("SHB_HINT_OWN", kEvictFirst);
-  p.serpentine = env_int("SHB_SERPENTINE", 1);
+  p.l2_hint_own = MODE == MODE_RS ? l2_policy("SHB_HINT_OWN_RS", kEvictNormal)
+                                   : l2_policy("SHB_HINT_OWN", kEvictFirst);
+  // 2: the serpentine parity continues across chunks (TP=8 proxy, ncu: RS DRAM
+  // reads 579 -> 505 MB, 349 -> 345 us; AG 423 -> 411 MB); = 1 at W = 1
+  p.serpentine = env_int("SHB_SERPENTINE", 2);
+  p.red_help = env_int("SHB_RED_HELP", 1);
   // K serpentine: AG C3 DRAM reads 484 -> 427 MB per launch; the RS grid
   // (C4: K = 3584, 17 tiles per cluster) reads more with it, so AG only
   p.kserp = env_int("SHB_KSERP", MODE == MODE_AG ? 1 : 0);
@@ -617,10 +621,24 @@ int check_shape(int m, int n, int k, int world, int dtype) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// The reduction is fused into the own chunk's epilogue unless the call is
-// phased (its tiles would wait on peers whose GEMM a serialising tool may
-// never run concurrently) or SHB_RS_UNFUSED=1 asks for the separate pass.
-bool rs_fused(int phase) { return phase == SH_PHASE_ALL && env_int("SHB_RS_UNFUSED", 0) == 0; }
+// Where the W-slot reduction runs.  At W = 1 it is fused into the epilogue
+// (one staging buffer feeds both stores).  At W > 1 the default is the
+// north star's "GEMM with a scattering epilogue, followed by a vectorised
+// in-HBM reduction": on the TP=8 proxy (ncu, one launch each) the GEMM with
+// every chunk in one raster region takes 292 us and the separate reduction
+// ~21 us, against 338 us for the GEMM whose own-chunk epilogues reduce --
+// those reductions compete with the last waves' operand streams and run at
+// a few warps per SM.  Ranks of one process that share a GPU keep the fused
+// form: a separate reduction kernel spinning on its peers' counters can take
+// the SMs a sibling rank's GEMM has not been granted yet (the persistent
+// grids are only co-resident if nothing else is queued between them).
+// Phased calls (serialising tools) are never fused.  SHB_RS_UNFUSED=1 / =0
+// forces either form (on shared GPUs too, for tests of the other form).
+bool rs_fused(int phase, int world, bool shares_gpu) {
+  if (phase != SH_PHASE_ALL) return false;
+  if (const char* e = getenv("SHB_RS_UNFUSED")) return atoi(e) == 0;
+  return world == 1 || shares_gpu;
+}
 
 }  // namespace
 
@@ -1530,7 +1548,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   CUDA_TRY(cudaSetDevice(rs->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device), rs->ranks_on_device, k);
-  const bool fuse = rs_fused(rs_phase);
+  const bool fuse = rs_fused(rs_phase, W, rs->shares_gpu);
   // With the reduction fused, the tiles of my own chunk wait for every peer's
   // rows; a cluster that reached them before finishing its peer-chunk tiles
   // would hold back rows a peer is waiting for, on every rank at once.  The
@@ -1584,6 +1602,16 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
   p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
+  // One raster region over every chunk that no epilogue waits behind (fused:
+  // the peer chunks, the own chunk stays last; unfused: all of them), so B
+  // is streamed once per raster group rather than once per chunk (C4 at
+  // TP=8: 8 x 58 MB of B).  The peers' chunks then complete together near the
+  // end of the region instead of one by one -- the owner waits for the last
+  // of them either way, at the start of its own chunk.  SHB_RS_MERGE=0: off.
+  p.merge = (W > 2 || (W == 2 && !fuse)) && env_int("SHB_RS_MERGE", 1) ? (fuse ? W - 1 : W) : 0;
+  if (p.merge > 1)
+    p.group_m_merged = raster_group(p.rows * p.merge, p.k, p.mblk * p.merge, 128 * cfg.cg,
+                                    cfg.grid / cfg.cg);
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);
@@ -1646,13 +1674,32 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   int grid = (int)std::min<size_t>((nvec + 255) / 256, (size_t)sms * 4);
   if (grid < 1) grid = 1;
   const uint64_t* counters = sig_addr(w, *rs, rank, reduction_base);
-  if (dtype == SH_DTYPE_FP16)
-    rs_reduce_kernel<true><<<grid, 256, 0, s>>>(staging, static_cast<uint16_t*>(out), slot_elems,
-                                                W, counters, target, rs->err_dev, w->timeout_ns);
-  else
-    rs_reduce_kernel<false><<<grid, 256, 0, s>>>(staging, static_cast<uint16_t*>(out), slot_elems,
-                                                 W, counters, target, rs->err_dev, w->timeout_ns);
-  CUDA_TRY(cudaGetLastError());
+  // Programmatic dependent launch: the reduction's CTAs may start while the
+  // GEMM still runs (it allows dependents right after its prologue) and
+  // take SMs as its CTAs retire.  No griddepcontrol.wait: every byte the
+  // reduction reads is covered by the element counters it acquires (the own
+  // slot's too), and the GEMM never touches `out` in this form.  Not for
+  // ranks sharing a GPU or phased calls (SHB_RED_PDL=0 / SHB_PDL=0: off).
+  const bool red_pdl = !rs->shares_gpu && rs_phase == SH_PHASE_ALL &&
+                       env_int("SHB_PDL", 1) != 0 && env_int("SHB_RED_PDL", 1) != 0;
+  {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid, 1, 1);
+    lc.blockDim = dim3(256, 1, 1);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = red_pdl ? 1 : 0;
+    uint16_t* o16 = static_cast<uint16_t*>(out);
+    if (dtype == SH_DTYPE_FP16)
+      CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<true>, staging, o16, slot_elems, W,
+                                  counters, target, rs->err_dev, w->timeout_ns));
+    else
+      CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<false>, staging, o16, slot_elems, W,
+                                  counters, target, rs->err_dev, w->timeout_ns));
+  }
 
   return store_flags(s, fl, nfl, epoch);
 }

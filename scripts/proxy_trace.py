@@ -39,6 +39,7 @@ try:
                 d["items"] += 1
             elif e["op"] == "tile_epilogue":
                 (d["epi_own"] if e["chunk"] == 0 and W > 1 else d["epi"]).append(e["t1_ns"] - e["t0_ns"])
+                d["last_acc"] = max(d.get("last_acc", 0), e["t0_ns"] - t0)
             elif e["op"] == "own_reduce":
                 d.setdefault("red", []).append(((e["t1_ns"] - e["t0_ns"]) / 1e3, e["drain_ns"] / 1e3))
             elif e["op"] == "cta":
@@ -56,6 +57,10 @@ try:
             "epi_own_us_median": statistics.median(allown) / 1e3 if allown else None,
             "epi_own_us_max": max(allown) / 1e3 if allown else None,
             "own_reduce_us": sorted(x for d in per.values() for x in d.get("red", []))[::16],
+            # tail: last accumulator ready (final MMA done) -> CTA end
+            "tail_us": sorted(round((d["end"] - d.get("last_acc", d["end"])) / 1e3, 1)
+                              for d in per.values() if "last_acc" in d)[::12],
+            "last_acc_us_max": max(d.get("last_acc", 0) for d in per.values()) / 1e3,
             "peer_wait_us_max": max((e["t1_ns"] - e["t0_ns"]) / 1e3 for e in ev
                                     if e["op"] == "peer_wait") if any(e["op"] == "peer_wait" for e in ev) else 0,
             "event_us": statistics.median(px.time_op(op, mode.rstrip("0"), 10, subchunks=1)),
