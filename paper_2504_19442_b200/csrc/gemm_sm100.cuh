@@ -39,8 +39,13 @@ struct TileParams {
   int mblk, nblk;  // m-blocks per chunk, n-blocks
   int num_tiles;   // world * mblk * nblk
   int group_m;     // raster group (m-blocks) for L2 reuse
-  int merge;       // leading chunk positions rastered as one region (<= 1: none)
-  int group_m_merged;  // raster group of that region
+  // raster regions: consecutive chunk positions [reg_s0[r], reg_s0[r+1])
+  // whose m-blocks form one raster (group reg_gm[r]; reg_g0[r] groups come
+  // before it).  nreg = 0: one region per position with group_m.
+  int nreg;
+  int reg_s0[kMaxWorld + 1];
+  int reg_gm[kMaxWorld];
+  int reg_g0[kMaxWorld];
   int serpentine;  // odd raster groups walk n backwards (2: parity continues across chunks)
   int kserp;       // every other data-parallel tile of a cluster walks K backwards
   int order[kMaxWorld];  // chunk visit order (reference swizzle.py)
@@ -282,30 +287,31 @@ struct TensorMaps {
 };
 
 // Tile t -> (chunk, m-block, n-block).  Tiles are enumerated position by
-// position of the chunk order; the first `merge` positions (RS: every peer
-// chunk, the own chunk staying last) may form ONE raster region whose
-// m-blocks are those of all its chunks, so a raster group spans several
-// chunks and B is streamed once per group instead of once per chunk.
+// position of the chunk order.  Consecutive positions may form ONE raster
+// region whose m-blocks are those of all its chunks (RS: every chunk no
+// epilogue waits behind; AG: pairs of chunks that have landed by the time
+// the consumer gets there), so a raster group spans several chunks and B is
+// streamed once per group instead of once per chunk.
 __device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chunk, int& mb,
                                             int& nb) {
   const int per_chunk = p.mblk * p.nblk;
-  const int merged = p.merge > 1 ? p.merge : 0;
-  int w, vblk, gm, s0, g0;  // index in region, its m-blocks, raster group, first position, groups before
-  if (t < merged * per_chunk) {
-    w = t;
-    vblk = merged * p.mblk;
-    gm = p.group_m_merged;
-    s0 = 0;
-    g0 = 0;
+  const int s = t / per_chunk;
+  int s0, np, gm, g0;  // region's first position, positions, raster group, groups before
+  if (p.nreg > 0) {
+    int r = 0;
+    while (r + 1 < p.nreg && p.reg_s0[r + 1] <= s) ++r;
+    s0 = p.reg_s0[r];
+    np = p.reg_s0[r + 1] - s0;
+    gm = p.reg_gm[r];
+    g0 = p.reg_g0[r];
   } else {
-    const int s = merged + (t - merged * per_chunk) / per_chunk;
-    w = t - s * per_chunk;
-    vblk = p.mblk;
-    gm = p.group_m;
     s0 = s;
-    const int gpre = merged ? (merged * p.mblk + p.group_m_merged - 1) / p.group_m_merged : 0;
-    g0 = gpre + (s - merged) * ((p.mblk + gm - 1) / gm);
+    np = 1;
+    gm = p.group_m;
+    g0 = s * ((p.mblk + gm - 1) / gm);
   }
+  const int w = t - s0 * per_chunk;
+  const int vblk = np * p.mblk;
   const int span = gm * p.nblk;
   const int group = w / span;
   const int first_m = group * gm;
@@ -313,7 +319,7 @@ __device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chu
   const int in = w - group * span;
   const int vm = first_m + in % gsize;
   nb = in / gsize;
-  const int vs = vm / p.mblk;  // chunk position inside a merged region (0 otherwise)
+  const int vs = vm / p.mblk;  // position inside the region
   chunk = p.order[s0 + vs];
   mb = vm - vs * p.mblk;
   // serpentine: odd groups walk the n-blocks backwards, so a group starts on

@@ -245,6 +245,21 @@ int raster_group(int rows, int k, int mblk, int bm, int clusters) {
   return (mblk + ngroups - 1) / ngroups;
 }
 
+// Raster regions of a launch (TileParams::reg_*): starts[0..nreg] are the
+// first chunk positions of each region, starts[nreg] = world.
+void set_regions(TileParams& p, const int* starts, int nreg, int bm, int clusters) {
+  p.nreg = nreg;
+  int g0 = 0;
+  for (int r = 0; r < nreg; ++r) {
+    const int np = starts[r + 1] - starts[r];
+    p.reg_s0[r] = starts[r];
+    p.reg_gm[r] = raster_group(p.rows * np, p.k, p.mblk * np, bm, clusters);
+    p.reg_g0[r] = g0;
+    g0 += (p.mblk * np + p.reg_gm[r] - 1) / p.reg_gm[r];
+  }
+  p.reg_s0[nreg] = starts[nreg];
+}
+
 Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1, int k = 0) {
   // ranks sharing one GPU split its SMs, so that all their persistent GEMMs
   // are co-resident (their epilogues wait on each other's stores)
@@ -1451,6 +1466,22 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
   p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
+  {
+    // Raster regions: the own chunk (position 0) and the first remote one
+    // alone, then SHB_AG_MERGE consecutive remote chunks per region (B
+    // streamed once per region).  The pushes run ahead of the consumer from
+    // the second remote chunk on (C3/TP=8: a 16 MB chunk lands every ~21 us,
+    // one chunk position of GEMM takes ~38 us), so a region's later chunks
+    // have landed when it opens.  Measured neutral on the TP=8 proxy (ncu:
+    // DRAM reads 412 / 408 / 445 MB, 305 / 305 / 306 us for 1 / 2 / 3; the
+    // cross-chunk serpentine already keeps B in L2), so default 1: regions
+    // are single chunks, and a chunk's tiles never wait on a later push.
+    const int mg = std::max(1, env_int("SHB_AG_MERGE", 1));
+    int starts[SH_MAX_WORLD + 1], nreg = 0;
+    for (int s0 = 0; s0 < W; s0 += (s0 < 2 ? 1 : mg)) starts[nreg++] = s0;
+    starts[nreg] = W;
+    set_regions(p, starts, nreg, 128 * cfg.cg, cfg.grid / cfg.cg);
+  }
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   p.ready = sig_addr(w, *rs, rank, ready_base);
@@ -1608,10 +1639,13 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   // TP=8: 8 x 58 MB of B).  The peers' chunks then complete together near the
   // end of the region instead of one by one -- the owner waits for the last
   // of them either way, at the start of its own chunk.  SHB_RS_MERGE=0: off.
-  p.merge = (W > 2 || (W == 2 && !fuse)) && env_int("SHB_RS_MERGE", 1) ? (fuse ? W - 1 : W) : 0;
-  if (p.merge > 1)
-    p.group_m_merged = raster_group(p.rows * p.merge, p.k, p.mblk * p.merge, 128 * cfg.cg,
-                                    cfg.grid / cfg.cg);
+  {
+    const int merge = env_int("SHB_RS_MERGE", 1) ? (fuse ? W - 1 : W) : 1;
+    int starts[SH_MAX_WORLD + 1], nreg = 0;
+    for (int s0 = 0; s0 < W; s0 += (s0 == 0 ? std::max(1, merge) : 1)) starts[nreg++] = s0;
+    starts[nreg] = W;
+    set_regions(p, starts, nreg, 128 * cfg.cg, cfg.grid / cfg.cg);
+  }
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);
