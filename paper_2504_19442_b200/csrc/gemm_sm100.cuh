@@ -980,9 +980,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (MODE == MODE_AG) {
               tma_store_3d_hint(&maps.c, sb, xcol, row, chunk, p.l2_hint_store);
             } else {
-              // own chunk at W > 1: re-read by the reduction right away
+              // own chunk at W > 1: re-read by the reduction (the fused
+              // epilogue's right away, the reduction kernel's at the end)
               tma_store_2d_hint(&maps.out[chunk], sb, xcol, row,
-                                fused_own && p.world > 1 ? p.l2_hint_own : p.l2_hint_store);
+                                chunk == p.rank && p.world > 1 ? p.l2_hint_own
+                                                               : p.l2_hint_store);
               if (dual) tma_store_3d_hint(&maps.c, sb, xcol, row, 0, p.l2_hint_store);
             }
             bulk_commit();
@@ -1106,9 +1108,9 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
                                                         const uint64_t* counters, uint64_t target,
                                                         int* err, uint64_t timeout_ns) {
   constexpr int kGroup = 8;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < world; ++s) spin_geq(counters + s, target, err, timeout_ns, 3);
-  }
+  // one thread per source acquires its counter (8 acquires in a row by one
+  // thread cost ~3 us per CTA at the kernel start: ncu 30.5 -> 27.4 us)
+  if ((int)threadIdx.x < world) spin_geq(counters + threadIdx.x, target, err, timeout_ns, 3);
   __syncthreads();
   // 16-byte vectors only when every slot starts 16-byte aligned
   const size_t nvec = (slot_elems % 8 == 0) ? slot_elems / 8 : 0;

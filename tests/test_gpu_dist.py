@@ -84,6 +84,10 @@ def _worker(rank, world, port, q):
             if hot:
                 why.append(f"it{it}: hot signals {hot}")
                 ok_rs = False
+            # the sweep reads this rank's pad: a faster peer must not start
+            # its next call (whose first act writes this rank's ready flag)
+            # before the sweep is done
+            dist.barrier()
         gathered = world_obj.read_tensor(rank, agb.gathered, torch.bfloat16, (256 * world, 128))
         ok_layout = np.array_equal(gathered.float().cpu().numpy(), oracle.gathered_layout(shards))
         dist.barrier()
