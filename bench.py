@@ -537,6 +537,17 @@ def main():
 
             proxy = tp_proxy.run(W=8, iters=20, peak_tflops=burst, ab=False)
             proxy["label"] = "tp8_proxy"
+            # the same per-rank kernels at TP=2 and TP=4 (C5's TP sweep on the
+            # C3/C4 shapes): preset / paced time and roofline fraction per op
+            lower = {}
+            for Wl in (2, 4):
+                r = tp_proxy.run(W=Wl, iters=8, peak_tflops=burst, ab=False)
+                lower[f"tp{Wl}"] = {
+                    "parity": r["parity"],
+                    **{op: {k: r[op][k] for k in ("preset_us", "paced_us", "tflops", "roofline_us",
+                                                  "roofline_frac", "speedup_vs_unfused_modelled")}
+                       for op in ("ag", "rs")}}
+            proxy["lower_tp"] = lower
         except Exception as e:  # noqa: BLE001 -- the proxy must never cost the headline line
             proxy = {"label": "tp8_proxy", "error": f"{type(e).__name__}: {e}"[:300]}
     dom_ms = ag_ms

@@ -451,5 +451,17 @@ if __name__ == "__main__":
     import json
     import sys
 
-    sys.stdout.write(json.dumps(run(iters=int(sys.argv[1]) if len(sys.argv) > 1 else 30,
-                                    peak_tflops=1700.9)) + "\n")
+    # python tp_proxy.py [iters] [W ...]: one JSON line per TP degree (the
+    # per-rank C3 / C4 shapes at TP=W: AG (8192, 28672/W, 8192), RS (8192,
+    # 8192, 28672/W)), peak = MEASURED_PEAKS.json burst bf16
+    import os
+
+    iters = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+    worlds = [int(x) for x in sys.argv[2:]] or [8]
+    peak = 1700.9
+    mp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        peak = json.load(open(mp)).get("bf16_tflops", peak)
+    for W in worlds:
+        sys.stdout.write(json.dumps(run(W=W, iters=iters, peak_tflops=peak, ab=False)) + "\n")
+        sys.stdout.flush()
