@@ -138,7 +138,11 @@ int stream_k_split(const Cfg& c, int num_kb) {
   if (c.bn == 512 && mode != 1) return c.tiles;
   const int waves = (c.tiles + clusters - 1) / clusters;
   const double eff = double(c.tiles) / double(waves * clusters);
-  const bool want = mode == 1 || (eff < 0.92 && num_kb >= 8);
+  // long K only: the split's fp32 partials and fixups cost a fixed amount
+  // per tile; measured on the TP proxy at M=1024 (ncu): RS k=3584 (56
+  // k-blocks) 72 -> 62 us and k=7168 104 -> 97 us without it, AG k=8192
+  // (128 k-blocks) 187 -> 162 us with it
+  const bool want = mode == 1 || (eff < 0.92 && num_kb >= 128);
   if (!want || c.tiles <= 0) return c.tiles;
   const int full = c.tiles / clusters;
   return full > 1 ? (full - 1) * clusters : 0;

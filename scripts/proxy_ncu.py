@@ -1,6 +1,6 @@
-"""ncu target: the TP=8 proxy's rank-0 kernels in preset mode (every flag set
+"""ncu target: the TP=W proxy's rank-0 kernels in preset mode (every flag set
 before the launch, so a kernel-serialising profiler cannot deadlock them).
-Usage: ncu ... python scripts/proxy_ncu.py [ag|rs|both] [W]"""
+Usage: ncu ... python scripts/proxy_ncu.py [ag|rs|both] [W] [M]"""
 import os
 import sys
 
@@ -9,7 +9,8 @@ import tp_proxy  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "both"
 W = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-px = tp_proxy.TpProxy(W, 8192, 28672 // W, 8192, 8192, 28672 // W)
+M = int(sys.argv[3]) if len(sys.argv) > 3 else 8192
+px = tp_proxy.TpProxy(W, M, 28672 // W, 8192, 8192, 28672 // W)
 try:
     for op in ("ag", "rs"):
         if which in (op, "both"):
