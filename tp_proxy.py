@@ -94,7 +94,11 @@ class TpProxy:
         self.c = torch.empty(m, n_ag, device=dev, dtype=bf)
         self.y = torch.empty(rows, n_rs, device=dev, dtype=bf)
         self.main = torch.cuda.Stream(device=dev)
-        self.feed = torch.cuda.Stream(device=dev)
+        # one feeder stream per peer: a stream memory op costs ~7 us of
+        # front-end time, so 7 releases queued on one stream could not be
+        # closer than that (small-M shards land every ~3 us)
+        self.feeds = [torch.cuda.Stream(device=dev) for _ in range(W)]
+        self.feed = self.feeds[0]
         # peers' data, placed once (see module doc)
         gath = w.heap_view(0, self.agb.gathered, bf, (W, rows, k_ag))
         stag = w.heap_view(0, self.rsb.staging, bf, (W, rows, n_rs))
@@ -107,7 +111,7 @@ class TpProxy:
         fs = ctypes.c_void_p(self.feed.cuda_stream)
         for base in (self.agb.done.base, self.rsb.producer.base):
             _lib.check(self.lib.sh_fill_signals(w.handle, 0, base, W, 1 << 62, fs))
-        self.feed.synchronize()
+        self._feeds_sync()
         # pinned words: [0] go (the host writes it once a call is fully
         # enqueued, so the timed region never holds host launch latency),
         # [1] origin (the main stream writes it right before a paced launch),
@@ -134,14 +138,19 @@ class TpProxy:
 
     def _release(self, rank_from, sig, value, tick):
         """Feeder: (wait for the pacer's tick) then set rank 0's signal word."""
-        fs = ctypes.c_void_p(self.feed.cuda_stream)
+        feed = self.feeds[rank_from % len(self.feeds)]
+        fs = ctypes.c_void_p(feed.cuda_stream)
         if tick is not None:
             _lib.check(self.lib.sh_stream_wait_word(self._word(2), tick, fs))
         _lib.check(self.lib.sh_signal_op(self.world.handle, rank_from, 0, sig, _lib.SH_SIG_SET, value, fs))
         if self.diag is not None:
             ev = torch.cuda.Event(enable_timing=True)
-            ev.record(self.feed)
+            ev.record(feed)
             self.diag.append(ev)
+
+    def _feeds_sync(self):
+        for f in self.feeds:
+            f.synchronize()
 
     def _call(self, mode, releases, launch):
         """One call: ``releases`` = [(rank_from, sig, value, delta_us)].
@@ -155,11 +164,13 @@ class TpProxy:
         ms = ctypes.c_void_p(self.main.cuda_stream)
         self._go += 1
         pacer, rc = None, []
-        self.feed.wait_stream(self.main)
+        for f in self.feeds:
+            f.wait_stream(self.main)
         if mode == "preset":
             for r_from, sig, val, _d in releases:
                 self._release(r_from, sig, val, None)
-            self.main.wait_stream(self.feed)
+            for f in self.feeds:
+                self.main.wait_stream(f)
         else:
             self._origin_val += 1
             base = self._tick
@@ -271,7 +282,7 @@ class TpProxy:
             if i >= warmup:
                 evs.append(ev)
         self.main.synchronize()
-        self.feed.synchronize()
+        self._feeds_sync()
         self.world.check_errors(0)
         return [a.elapsed_time(b) * 1e3 for a, b in evs]  # us
 
@@ -284,7 +295,7 @@ class TpProxy:
             start, end = (self._ag_call("paced", subchunks, kernel) if op == "ag"
                           else self._rs_call("paced", kernel))
             self.main.synchronize()
-            self.feed.synchronize()
+            self._feeds_sync()
             self.world.check_errors(0)
             return {"kernel_us": start.elapsed_time(end) * 1e3,
                     "released_us": [round(start.elapsed_time(ev) * 1e3, 1) for ev in self.diag]}
@@ -302,7 +313,7 @@ class TpProxy:
             self.diag = []
             try:
                 start, _end = self._call("paced", rel, None)
-                self.feed.synchronize()
+                self._feeds_sync()
                 self.main.synchronize()
                 late += [start.elapsed_time(ev) * 1e3 - d for ev, (*_x, d) in zip(self.diag, rel)]
             finally:
@@ -313,7 +324,7 @@ class TpProxy:
         self.diag = []
         try:
             start, _end = self._call("paced", rel, None)
-            self.feed.synchronize()
+            self._feeds_sync()
             self.main.synchronize()
             err = [start.elapsed_time(ev) * 1e3 - d for ev, (*_x, d) in zip(self.diag, rel)]
         finally:
