@@ -43,6 +43,10 @@ struct TileParams {
   // whose m-blocks form one raster (group reg_gm[r]; reg_g0[r] groups come
   // before it).  nreg = 0: one region per position with group_m.
   int nreg;
+  // RS with chunks of <= 128 rows (TP=8 at M=1024), every chunk in one
+  // region: the two CTAs of a pair tile take two consecutive chunk
+  // positions (128 rows each), instead of a 256-row tile half padding
+  int pair_chunks;
   int reg_s0[kMaxWorld + 1];
   int reg_gm[kMaxWorld];
   int reg_g0[kMaxWorld];
@@ -293,7 +297,23 @@ struct TensorMaps {
 // the consumer gets there), so a raster group spans several chunks and B is
 // streamed once per group instead of once per chunk.
 __device__ __forceinline__ void decode_tile(const TileParams& p, int t, int& chunk, int& mb,
-                                            int& nb) {
+                                            int& nb, uint32_t cta_rank = 0) {
+  if (p.pair_chunks) {
+    // one region of W/2 chunk pairs; group_m counts pairs
+    const int vblk = p.world / 2;
+    const int gm = p.group_m;
+    const int span = gm * p.nblk;
+    const int group = t / span;
+    const int first_m = group * gm;
+    const int gsize = min(vblk - first_m, gm);
+    const int in = t - group * span;
+    const int vm = first_m + in % gsize;
+    nb = in / gsize;
+    if (p.serpentine && (group & 1)) nb = p.nblk - 1 - nb;
+    chunk = p.order[2 * vm + (int)cta_rank];
+    mb = 0;
+    return;
+  }
   const int per_chunk = p.mblk * p.nblk;
   const int s = t / per_chunk;
   int s0, np, gm, g0;  // region's first position, positions, raster group, groups before
@@ -598,13 +618,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool wave_lead = p.wave_flags != nullptr && leader;
       while (wi.next(w)) {
         int chunk, mb, nb;
-        decode_tile(p, w.t, chunk, mb, nb);
+        decode_tile(p, w.t, chunk, mb, nb, cta_rank);
         const bool dp_item = w.t < p.dp_tiles;
         if (wave_lead && dp_item && waves_issued > 0)
           wave_wait(p.wave_flags, p.wave_tag, waves_issued, num_clusters, p.dp_tiles);
         const bool own = (MODE == MODE_AG) && chunk == p.rank;
         const bool copying = own && p.copy_own;
-        const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
+        const int row0 = p.pair_chunks ? 0 : mb * (BM * CG) + (int)cta_rank * BM;
         const int col0 = nb * BN + (int)cta_rank * BNC;
         // global column of this CTA's B box j: for BN <= 256 the CTA holds
         // the contiguous half [col0, col0 + BNC); for BN = 512 it holds the
@@ -833,10 +853,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     WorkItem w;
     for (; wi.next(w); ++it) {
       int chunk, mb, nb;
-      decode_tile(p, w.t, chunk, mb, nb);
+      decode_tile(p, w.t, chunk, mb, nb, cta_rank);
       const int as = C::NACC == 2 ? (it & 1) : 0;
       const uint32_t aphase = C::NACC == 2 ? ((it >> 1) & 1) : (it & 1);
-      const int cta_row0 = mb * (BM * CG) + (int)cta_rank * BM;
+      const int cta_row0 = p.pair_chunks ? 0 : mb * (BM * CG) + (int)cta_rank * BM;
       const int row = cta_row0 + q * 32;  // first row of this warp's slab
       const int n0 = nb * BN;
       const bool fused_own = (MODE == MODE_RS) && p.fuse_reduce && chunk == p.rank;

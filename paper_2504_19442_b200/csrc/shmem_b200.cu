@@ -1584,6 +1584,18 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Cfg cfg = choose_cfg(rows, W, n, num_sms(rs->device), rs->ranks_on_device, k);
   const bool fuse = rs_fused(rs_phase, W, rs->shares_gpu);
+  // Chunks of <= 128 rows (TP=8 at M=1024) with every chunk in one raster
+  // region (no fused reduction): a pair tile's two CTAs take two consecutive
+  // chunk positions, 128 rows each, instead of 1-CTA tiles (ncu, RS
+  // 1024x8192x3584 at TP=8: see DESIGN).  SHB_RS_PAIR_CHUNKS=0: off.
+  const bool pair_chunks = !fuse && W % 2 == 0 && rows <= 128 && cfg.cg == 1 &&
+                           !g_force_bn && !g_force_cg && env_int("SHB_RS_PAIR_CHUNKS", 1) != 0;
+  if (pair_chunks) {
+    int sms = num_sms(rs->device);
+    if (rs->ranks_on_device > 1) sms = std::max(2, (sms / rs->ranks_on_device) & ~1);
+    const int nblk = (n + 255) / 256, tiles = (W / 2) * nblk;
+    cfg = Cfg{256, 2, std::min(tiles, sms / 2) * 2, 1, nblk, tiles};
+  }
   // With the reduction fused, the tiles of my own chunk wait for every peer's
   // rows; a cluster that reached them before finishing its peer-chunk tiles
   // would hold back rows a peer is waiting for, on every rank at once.  The
@@ -1636,7 +1648,9 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
+  p.group_m = pair_chunks ? raster_group(p.rows * W, p.k, W / 2, 256, cfg.grid / cfg.cg)
+                          : raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
+  p.pair_chunks = pair_chunks ? 1 : 0;
   // One raster region over every chunk that no epilogue waits behind (fused:
   // the peer chunks, the own chunk stays last; unfused: all of them), so B
   // is streamed once per raster group rather than once per chunk (C4 at

@@ -75,3 +75,26 @@ def test_tp8_ag_product_and_layout(proxy):
     assert _rel(proxy.c, ref) <= TOL
     g = proxy.world.heap_view(0, proxy.agb.gathered, torch.bfloat16, (proxy.W * proxy.rows, proxy.ag.k))
     assert torch.equal(g, proxy.x.reshape(-1, proxy.ag.k))
+
+
+@pytest.mark.parametrize("W,M", [(8, 1024), (4, 512), (2, 256)])
+def test_small_chunk_rs_pair_tiles_bits(W, M):
+    # chunks of <= 128 rows: the scattering GEMM pairs two chunk positions per
+    # CTA pair (SHB_RS_PAIR_CHUNKS); same bits as the ascending-source sum,
+    # staging slot 0 within tolerance, for a world whose chunk count is even
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import tp_proxy
+
+    px = tp_proxy.TpProxy(W, M, 28672 // W, 8192, 8192, 28672 // W, timeout_s=30.0)
+    try:
+        for mode in ("preset", "paced"):
+            px.y.fill_(float("nan"))
+            px.time_op("rs", mode, 1, warmup=1)
+            torch.cuda.synchronize()
+            stag, ref = _ascending_sum(px)
+            assert torch.equal(px.y.view(torch.int16), ref.view(torch.int16))
+            part = px.a_rs[: px.rows].float() @ px.b_rs.float()
+            assert _rel(stag[0], part) <= TOL
+    finally:
+        px.close()
