@@ -43,9 +43,9 @@ struct TileParams {
   // whose m-blocks form one raster (group reg_gm[r]; reg_g0[r] groups come
   // before it).  nreg = 0: one region per position with group_m.
   int nreg;
-  // RS with chunks of <= 128 rows (TP=8 at M=1024), every chunk in one
-  // region: the two CTAs of a pair tile take two consecutive chunk
-  // positions (128 rows each), instead of a 256-row tile half padding
+  // chunks of <= 128 rows (TP=8 at M=1024): the two CTAs of a pair tile
+  // take two consecutive chunk positions (128 rows each) instead of 1-CTA
+  // tiles (a 256-row tile would be half padding); one raster over the pairs
   int pair_chunks;
   int reg_s0[kMaxWorld + 1];
   int reg_gm[kMaxWorld];
@@ -799,9 +799,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       WorkItem w;
       while (wi.next(w)) {
         int chunk, mb, nb;
-        decode_tile(p, w.t, chunk, mb, nb);
+        decode_tile(p, w.t, chunk, mb, nb, cta_rank);
         const bool copying = chunk == p.rank;
-        const int row0 = mb * (BM * CG) + (int)cta_rank * BM;
+        const int row0 = p.pair_chunks ? 0 : mb * (BM * CG) + (int)cta_rank * BM;
         const bool dp_item = w.t < p.dp_tiles;
         const bool rev = p.kserp && w.kind == 0 && dp_item && (dp_seen & 1);
         if (dp_item) ++dp_seen;

@@ -1385,6 +1385,17 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = rs->device;
   Cfg cfg = choose_cfg(rows, W, n, num_sms(dev), rs->ranks_on_device, k);
+  // chunks of <= 128 rows: pair tiles over two chunk positions (as in the
+  // RS, TileParams::pair_chunks); the own chunk shares its pairs' first
+  // tiles with the first remote chunk.  SHB_AG_PAIR_CHUNKS=0: off.
+  const bool pair_chunks = W % 2 == 0 && rows <= 128 && cfg.cg == 1 && !g_force_bn &&
+                           !g_force_cg && env_int("SHB_AG_PAIR_CHUNKS", 1) != 0;
+  if (pair_chunks) {
+    int sms = num_sms(dev);
+    if (rs->ranks_on_device > 1) sms = std::max(2, (sms / rs->ranks_on_device) & ~1);
+    const int nblk = (n + 255) / 256, tiles = (W / 2) * nblk;
+    cfg = Cfg{256, 2, std::min(tiles, sms / 2) * 2, 1, nblk, tiles};
+  }
   const bool own_by_ce = env_int("SHB_OWN_COPY_CE", 0) != 0;
   const bool do_comm = phase != SH_PHASE_COMPUTE;
   const bool do_compute = phase != SH_PHASE_COMM;
@@ -1469,7 +1480,9 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   p.mblk = cfg.mblk;
   p.nblk = cfg.nblk;
   p.num_tiles = cfg.tiles;
-  p.group_m = raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
+  p.group_m = pair_chunks ? raster_group(p.rows * W, p.k, W / 2, 256, cfg.grid / cfg.cg)
+                          : raster_group(p.rows, p.k, p.mblk, 128 * cfg.cg, cfg.grid / cfg.cg);
+  p.pair_chunks = pair_chunks ? 1 : 0;
   {
     // Raster regions: the own chunk (position 0) and the first remote one
     // alone, then SHB_AG_MERGE consecutive remote chunks per region (B

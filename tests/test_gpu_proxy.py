@@ -78,7 +78,7 @@ def test_tp8_ag_product_and_layout(proxy):
 
 
 @pytest.mark.parametrize("W,M", [(8, 1024), (4, 512), (2, 256)])
-def test_small_chunk_rs_pair_tiles_bits(W, M):
+def test_small_chunk_pair_tiles_bits(W, M):
     # chunks of <= 128 rows: the scattering GEMM pairs two chunk positions per
     # CTA pair (SHB_RS_PAIR_CHUNKS); same bits as the ascending-source sum,
     # staging slot 0 within tolerance, for a world whose chunk count is even
@@ -96,5 +96,13 @@ def test_small_chunk_rs_pair_tiles_bits(W, M):
             assert torch.equal(px.y.view(torch.int16), ref.view(torch.int16))
             part = px.a_rs[: px.rows].float() @ px.b_rs.float()
             assert _rel(stag[0], part) <= TOL
+            # the AG with the same pairing: product and gathered layout
+            px.c.fill_(float("nan"))
+            px.time_op("ag", mode, 1, warmup=1)
+            torch.cuda.synchronize()
+            ref_ag = px.x.reshape(-1, px.ag.k).float() @ px.b_ag.float()
+            assert _rel(px.c, ref_ag) <= TOL
+            g = px.world.heap_view(0, px.agb.gathered, torch.bfloat16, (px.W * px.rows, px.ag.k))
+            assert torch.equal(g, px.x.reshape(-1, px.ag.k))
     finally:
         px.close()
