@@ -26,7 +26,8 @@ for a in sys.argv[4:]:
     env = dict(kv.split(":", 1) for kv in spec.split(",") if kv)
     cfgs.append((label, env))
 
-px = tp_proxy.TpProxy(W, 8192, 28672 // W, 8192, 8192, 28672 // W)
+M = int(os.environ.get("PROXY_M", "8192"))
+px = tp_proxy.TpProxy(W, M, 28672 // W, 8192, 8192, 28672 // W)
 res = {}
 try:
     base_env = {k: os.environ.get(k) for _, e in cfgs for k in e}
