@@ -740,3 +740,38 @@ def test_graph_capture_refused_loudly(rng):
         # the library still works after the refused captures
         out = ag_gemm(pe, a, b, shape, ag_order_switch(0, 1), agb)
         assert np.array_equal(to_np(out), to_np(a) @ to_np(b))
+
+
+@pytest.mark.parametrize("world_size,rows,n,k", [(2, 128, 264, 200), (4, 72, 512, 136),
+                                                 (4, 128, 256, 520), (8, 40, 136, 72)])
+@pytest.mark.parametrize("unfused", ["0", "1"])
+def test_pair_chunk_tiles_exact(rng, monkeypatch, world_size, rows, n, k, unfused):
+    # chunks of <= 128 rows in an even world: a CTA pair takes two chunk
+    # positions (AG always; RS when the reduction is a separate pass), incl.
+    # ragged rows / n / k; outputs and both layouts bit-exact
+    monkeypatch.setenv("SHB_RS_UNFUSED", unfused)
+    m = rows * world_size
+    shape = ProblemShape(m=m, n=n, k=k, dtype="bfloat16")
+    with make_world(world_size, heap_bytes=1 << 26) as w:
+        agb, rsb = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+        shards = [ints(rng, -2, 3, (rows, k)) for _ in range(world_size)]
+        amats = [ints(rng, -1, 2, (m, k)) for _ in range(world_size)]
+        b = ints(rng, -1, 2, (k, n))
+        ag_ref = oracle.ag_gemm_reference(shards, b)
+        rs_ref = oracle.gemm_rs_reference(amats, [b] * world_size)
+
+        def body(pe):
+            x, a, bb = dev(shards[pe.rank], pe), dev(amats[pe.rank], pe), dev(b, pe)
+            h = ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, world_size), agb, reset=False)
+            y = gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, world_size), rsb, reset=False)
+            return h, y
+
+        for _ in range(2):  # back to back: epochs advance, no reset
+            for r, (h, y) in enumerate(run_np(w, body)):
+                assert np.array_equal(h, ag_ref)
+                assert np.array_equal(y, rs_ref[r])
+        for r in range(world_size):
+            staging = to_np(w.read_tensor(r, rsb.staging, BF16, (world_size, rows, n)))
+            assert np.array_equal(staging, oracle.staging_layout(amats, [b] * world_size, r))
+            gathered = to_np(w.read_tensor(r, agb.gathered, BF16, (m, k)))
+            assert np.array_equal(gathered, oracle.gathered_layout(shards))
