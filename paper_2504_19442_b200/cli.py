@@ -41,7 +41,7 @@ _DESCRIPTIONS = {
     "reducescatter": "push-mode ReduceScatter (int64) vs the dense sum",
     "ag-gemm": "fused AllGather+GEMM (bf16 exact ints) vs vstack(shards) @ b",
     "gemm-rs": "fused GEMM+ReduceScatter (bf16 exact ints) vs row blocks of sum A_r @ B",
-    "ag-gemm-tile": "tune the AG+GEMM kernel knobs (bn, stream_k, group_m) on device time",
+    "ag-gemm-tile": "tune the AG+GEMM kernel knobs (bn, stream_k, group_m, subchunks, ...) on device time",
 }
 
 

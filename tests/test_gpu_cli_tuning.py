@@ -40,3 +40,19 @@ def test_tune_ag_gemm_tile(tmp_path, capsys):
     report = json.loads((tmp_path / "ag-gemm-tile_report.json").read_text())
     assert len(report["configs"]) == 4 and all(sc > 0 for sc in report["scores"])
     assert report["per_rank_chosen"] == [report["chosen_index"]] * 2
+
+
+def test_tune_subchunk_and_reduction_knobs(tmp_path, capsys):
+    # the ag-gemm-tile scenario over the sub-chunking knob (AG) on a W=2
+    # world; every candidate runs bit-exact and the choice is unanimous
+    doc = {"scenario": "ag-gemm-tile", "world": {"world_size": 2, "heap_bytes": 1 << 26},
+           "problem": {"m": 1024, "n": 512, "k": 512}, "iterations": 2,
+           "axes": {"subchunks": [0, 2], "rs_reduce": ["auto", "separate"]}}
+    p = tmp_path / "t.json"
+    p.write_text(json.dumps(doc))
+    rc = cli.main(["tune", "--config", str(p), "--out", str(tmp_path)])
+    out = json.loads(capsys.readouterr().out)
+    assert rc == cli.EXIT_OK, out
+    report = json.loads((tmp_path / "ag-gemm-tile_report.json").read_text())
+    assert len(report["configs"]) == 4 and all(sc and sc > 0 for sc in report["scores"])
+    assert report["per_rank_chosen"] == [report["chosen_index"]] * 2

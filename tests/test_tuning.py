@@ -134,3 +134,24 @@ def test_report_json_roundtrip():
     r = TuneReport({"x": [0]}, [{"x": 0}], [[[1.0]]], [1.0], 0, {"x": 0}, [0], {})
     doc = json.loads(r.to_json())
     assert doc["chosen_config"] == {"x": 0} and doc["invalid"] == {}
+
+
+def test_kernel_config_environment_knobs_restore(monkeypatch):
+    # the sub-chunking and reduction-form knobs travel through the library's
+    # environment for the block and are restored afterwards
+    import os
+
+    from paper_2504_19442_b200 import ConfigurationError
+    from paper_2504_19442_b200.tuning import kernel_config
+
+    monkeypatch.setenv("SHB_AG_SUB", "2")
+    monkeypatch.delenv("SHB_RS_UNFUSED", raising=False)
+    with kernel_config(subchunks=4, rs_reduce="separate"):
+        assert os.environ["SHB_AG_SUB"] == "4" and os.environ["SHB_RS_UNFUSED"] == "1"
+    assert os.environ["SHB_AG_SUB"] == "2" and "SHB_RS_UNFUSED" not in os.environ
+    with kernel_config(subchunks=0, rs_reduce="fused"):
+        assert "SHB_AG_SUB" not in os.environ and os.environ["SHB_RS_UNFUSED"] == "0"
+    assert os.environ["SHB_AG_SUB"] == "2"
+    with pytest.raises(ConfigurationError):
+        with kernel_config(rs_reduce="sometimes"):
+            pass
