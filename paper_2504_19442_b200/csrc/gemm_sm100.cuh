@@ -1126,12 +1126,24 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
                                                         uint16_t* __restrict__ out,
                                                         size_t slot_elems, int world,
                                                         const uint64_t* counters, uint64_t target,
-                                                        int* err, uint64_t timeout_ns) {
+                                                        int* err, uint64_t timeout_ns,
+                                                        uint64_t* trace, int trace_cap,
+                                                        int trace_grid) {
   constexpr int kGroup = 8;
+  const bool tracer = trace != nullptr && threadIdx.x == 0 && (int)blockIdx.x < trace_grid &&
+                      trace_cap >= 2;
+  const uint64_t t0 = tracer ? globaltimer() : 0;
   // one thread per source acquires its counter (8 acquires in a row by one
   // thread cost ~3 us per CTA at the kernel start: ncu 30.5 -> 27.4 us)
   if ((int)threadIdx.x < world) spin_geq(counters + threadIdx.x, target, err, timeout_ns, 3);
   __syncthreads();
+  if (tracer) {  // kind 3: waiting for the peers' rows (the exposed part of the RS)
+    uint64_t* r = trace + (size_t)blockIdx.x * trace_cap * 4;
+    r[0] = 3ull << 56;
+    r[1] = t0;
+    r[2] = globaltimer();
+    r[3] = 0;
+  }
   // 16-byte vectors only when every slot starts 16-byte aligned
   const size_t nvec = (slot_elems % 8 == 0) ? slot_elems / 8 : 0;
   const uint4* st = reinterpret_cast<const uint4*>(staging);
@@ -1172,6 +1184,13 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
     }
     out[i] = FP16 ? __half_as_ushort(__float2half_rn(acc))
                   : __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+  }
+  if (tracer) {  // kind 4: the CTA's lifetime
+    uint64_t* r = trace + ((size_t)blockIdx.x * trace_cap + 1) * 4;
+    r[0] = (4ull << 56) | blockIdx.x;
+    r[1] = t0;
+    r[2] = globaltimer();
+    r[3] = 0;
   }
 }
 

@@ -616,14 +616,24 @@ void attach_wave(RS& rs, TileParams& p) {
   p.wave_tag = (++rs.wave_epoch) << 32;
 }
 
+// Next slot of the rank's trace ring for a launch of `mode` (0 AG GEMM, 1 RS
+// GEMM, 2 RS reduction kernel), cleared on the launch stream first so a
+// reused slot holds no records of an older launch.  nullptr: not tracing.
 template <typename RS>
-void attach_trace(RS& rs, TileParams& p, int mode) {
-  if (!rs.trace) return;
+uint64_t* trace_slot(RS& rs, int mode, cudaStream_t s) {
+  if (!rs.trace) return nullptr;
   const int slot = (int)(rs.trace_count % rs.trace_launches);
-  p.trace = rs.trace + (size_t)slot * rs.trace_grid * rs.trace_cap * 4;
-  p.trace_cap = rs.trace_cap;
+  uint64_t* base = rs.trace + (size_t)slot * rs.trace_grid * rs.trace_cap * 4;
+  cudaMemsetAsync(base, 0, (size_t)rs.trace_grid * rs.trace_cap * 4 * 8, s);
   rs.trace_modes[slot] = mode;
   ++rs.trace_count;
+  return base;
+}
+
+template <typename RS>
+void attach_trace(RS& rs, TileParams& p, int mode, cudaStream_t s) {
+  p.trace = trace_slot(rs, mode, s);
+  p.trace_cap = p.trace ? rs.trace_cap : 0;
 }
 
 int check_shape(int m, int n, int k, int world, int dtype) {
@@ -1504,7 +1514,7 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   p.ready = sig_addr(w, *rs, rank, ready_base);
   p.ag_sub = S_eff;
   p.ag_sub_rows = sub_rows;
-  attach_trace(*rs, p, MODE_AG);
+  attach_trace(*rs, p, MODE_AG, s);
   if (dynamic_tiles()) {
     p.tile_counter = rs->tile_counter;
     if ((rc = zero_counter(rs->tile_counter, s))) return rc;
@@ -1705,7 +1715,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
       p.ws_epoch = ++rs->sk.epoch;
     }
   }
-  attach_trace(*rs, p, MODE_RS);
+  attach_trace(*rs, p, MODE_RS, s);
   if (dynamic_tiles()) {
     p.tile_counter = rs->tile_counter;
     if ((rc = zero_counter(rs->tile_counter, s))) return rc;
@@ -1758,12 +1768,15 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
     lc.attrs = at;
     lc.numAttrs = red_pdl ? 1 : 0;
     uint16_t* o16 = static_cast<uint16_t*>(out);
+    // timeline: per CTA (< trace grid) its counter wait (kind 3) and life (kind 4)
+    uint64_t* tr = trace_slot(*rs, 2, s);
+    const int tcap = tr ? rs->trace_cap : 0, tgrid = tr ? rs->trace_grid : 0;
     if (dtype == SH_DTYPE_FP16)
       CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<true>, staging, o16, slot_elems, W,
-                                  counters, target, rs->err_dev, w->timeout_ns));
+                                  counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid));
     else
       CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<false>, staging, o16, slot_elems, W,
-                                  counters, target, rs->err_dev, w->timeout_ns));
+                                  counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid));
   }
 
   return store_flags(s, fl, nfl, epoch);

@@ -23,7 +23,7 @@ from . import _lib
 
 _KINDS = {1: "chunk_wait", 2: "tile_epilogue", 3: "peer_wait", 4: "cta", 5: "mma_item",
           6: "own_reduce"}
-_MODES = {0: "ag_gemm", 1: "gemm_rs"}
+_MODES = {0: "ag_gemm", 1: "gemm_rs", 2: "rs_reduce"}
 
 
 def start_trace(world, records_per_cta=512, launches=16):

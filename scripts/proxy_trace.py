@@ -26,7 +26,9 @@ try:
         px.world.start_trace(records_per_cta=1024, launches=2)
         px.time_op(op, mode.rstrip("0"), 1, warmup=0, subchunks=1)
         ev = px.world.stop_trace()
-        last = max(e["launch"] for e in ev)
+        kern = "ag_gemm" if op == "ag" else "gemm_rs"
+        last = max(e["launch"] for e in ev if e["kernel"] == kern)
+        red = [e for e in ev if e["kernel"] == "rs_reduce" and e["launch"] > last]
         ev = [e for e in ev if e["launch"] == last]
         t0 = min(e["t0_ns"] for e in ev if e["op"] == "cta")
         per = {}
@@ -63,6 +65,13 @@ try:
             "last_acc_us_max": max(d.get("last_acc", 0) for d in per.values()) / 1e3,
             "peer_wait_us_max": max((e["t1_ns"] - e["t0_ns"]) / 1e3 for e in ev
                                     if e["op"] == "peer_wait") if any(e["op"] == "peer_wait" for e in ev) else 0,
+            # separate RS reduction kernel: its CTAs' wait for the peers'
+            # rows (kind 3) after the GEMM, and its span
+            "reduce_wait_us_max": max(((e["t1_ns"] - e["t0_ns"]) / 1e3 for e in red
+                                       if e["op"] == "peer_wait"), default=None),
+            "reduce_span_us": ((max(e["t1_ns"] for e in red if e["op"] == "cta")
+                                - min(e["t0_ns"] for e in red if e["op"] == "cta")) / 1e3
+                               if any(e["op"] == "cta" for e in red) else None),
             "event_us": statistics.median(px.time_op(op, mode.rstrip("0"), 10, subchunks=1)),
         }
 finally:

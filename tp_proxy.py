@@ -262,7 +262,8 @@ class TpProxy:
             self.time_op("rs", "preset", 1, warmup=0)
         finally:
             ev = self.world.stop_trace()
-        last = max(e["launch"] for e in ev if e["rank"] == 0)
+        # the GEMM's launch (the separate reduction kernel is traced too)
+        last = max(e["launch"] for e in ev if e["rank"] == 0 and e["kernel"] == "gemm_rs")
         ev = [e for e in ev if e["rank"] == 0 and e["launch"] == last]
         t0 = min(e["t0_ns"] for e in ev if e["op"] == "cta")
         end = {}
