@@ -512,23 +512,12 @@ def main():
     barrier()
     pcie_ms = max_over_ranks(p0.elapsed_time(p1) / 5)
 
-    cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        cb = cpu_measure(steps=5, warmup=1, budget_s=20.0)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-
     # ------------------------------------------------------------- roofline
     burst, sustained, peak_src = peaks()
-    sweep = None
-    if not args.no_sweep:
-        # short calls (a few ms each): the burst peak is the roofline denominator
-        try:
-            sweep = run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, burst,
-                              sustained)
-            world.check_errors(rank)
-        except Exception as e:  # noqa: BLE001 -- the sweep must never cost the headline line
-            sweep = {"error": f"{type(e).__name__}: {e}"[:300]}
     proxy = None
+    # (before the CPU baseline -- its BLAS threads compete with the proxy's
+    # host pacer -- and the C5 sweep, which heats the GPU past the state of
+    # the burst peak that is the proxy's roofline denominator)
     if rank == 0 and N == 1 and not args.no_proxy:
         # rank 0 of TP=8 at the C3/C4 per-rank shapes, peers emulated on this
         # GPU (tp_proxy.py); not a scaling number -- SCALE runs measure N>1
@@ -550,6 +539,20 @@ def main():
             proxy["lower_tp"] = lower
         except Exception as e:  # noqa: BLE001 -- the proxy must never cost the headline line
             proxy = {"label": "tp8_proxy", "error": f"{type(e).__name__}: {e}"[:300]}
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        cb = cpu_measure(steps=5, warmup=1, budget_s=20.0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    sweep = None
+    if not args.no_sweep:
+        # short calls (a few ms each): the burst peak is the roofline denominator
+        try:
+            sweep = run_sweep(sb, world, pe, N, dev, stream, barrier, max_over_ranks, burst,
+                              sustained)
+            world.check_errors(rank)
+        except Exception as e:  # noqa: BLE001 -- the sweep must never cost the headline line
+            sweep = {"error": f"{type(e).__name__}: {e}"[:300]}
     dom_ms = ag_ms
     achieved = flops(AG) / (dom_ms * 1e-3) / 1e12
     # the roofline call is timed right after K back-to-back steps: under the
