@@ -1194,6 +1194,91 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
   }
 }
 
+// The same reduction with the W source slots staged by bulk copies (the DMA
+// path of TMA, no tensor map): each step a CTA pulls 4 KB of every source
+// into shared memory (kRbStages-deep ring on mbarriers), and each thread sums
+// one 16-byte vector across the sources in ascending order -- the load side
+// becomes a few large DMA requests instead of W x 256 16-byte loads per step.
+constexpr int kRbChunk = 4096;  // bytes of one source per step (256 threads x 16 B)
+
+template <bool FP16>
+__global__ void __launch_bounds__(256) rs_reduce_bulk_kernel(
+    const uint16_t* __restrict__ staging, uint16_t* __restrict__ out, size_t slot_elems, int world,
+    int stages, const uint64_t* counters, uint64_t target, int* err, uint64_t timeout_ns,
+    uint64_t* trace, int trace_cap, int trace_grid) {
+  extern __shared__ uint8_t rb_raw[];
+  uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rb_raw) + 127) &
+                                            ~uintptr_t(127));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(buf + (size_t)stages * world * kRbChunk);
+  const bool tracer = trace != nullptr && threadIdx.x == 0 && (int)blockIdx.x < trace_grid &&
+                      trace_cap >= 2;
+  const uint64_t t0 = tracer ? globaltimer() : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if ((int)threadIdx.x < world) spin_geq(counters + threadIdx.x, target, err, timeout_ns, 3);
+  __syncthreads();
+  if (tracer) {  // kind 3: waiting for the peers' rows
+    uint64_t* r = trace + (size_t)blockIdx.x * trace_cap * 4;
+    r[0] = 3ull << 56;
+    r[1] = t0;
+    r[2] = globaltimer();
+    r[3] = 0;
+  }
+  const size_t slot_bytes = slot_elems * 2;
+  const long long nchunks = (long long)((slot_bytes + kRbChunk - 1) / kRbChunk);
+  const char* src0 = reinterpret_cast<const char*>(staging);
+  auto issue = [&](long long i) {  // thread 0: step i of this CTA into stage i % stages
+    const long long c = blockIdx.x + i * (long long)gridDim.x;
+    if (c >= nchunks) return;
+    const int st = (int)(i % stages);
+    const uint32_t bytes = (uint32_t)min((size_t)kRbChunk, slot_bytes - (size_t)c * kRbChunk);
+    mbar_arrive_expect_tx(&bars[st], bytes * (uint32_t)world);
+    for (int s = 0; s < world; ++s)
+      bulk_load_g2s(buf + ((size_t)st * world + s) * kRbChunk,
+                    src0 + (size_t)s * slot_bytes + (size_t)c * kRbChunk, bytes, &bars[st]);
+  };
+  const long long steps = nchunks > (long long)blockIdx.x
+                              ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0)
+    for (long long i = 0; i < stages && i < steps; ++i) issue(i);
+  for (long long i = 0; i < steps; ++i) {
+    const int st = (int)(i % stages);
+    mbar_wait(&bars[st], (uint32_t)((i / stages) & 1));
+    const long long c = blockIdx.x + i * (long long)gridDim.x;
+    const size_t off = (size_t)c * kRbChunk + (size_t)threadIdx.x * 16;
+    if (off < slot_bytes) {
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      for (int s = 0; s < world; ++s) {
+        const uint4 v = *reinterpret_cast<const uint4*>(buf + ((size_t)st * world + s) * kRbChunk +
+                                                        threadIdx.x * 16);
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = unpack2(w4[e], FP16);
+          acc[2 * e] += f.x;
+          acc[2 * e + 1] += f.y;
+        }
+      }
+      __stcs(reinterpret_cast<uint4*>(reinterpret_cast<char*>(out) + off),
+             make_uint4(pack2(acc[0], acc[1], FP16), pack2(acc[2], acc[3], FP16),
+                        pack2(acc[4], acc[5], FP16), pack2(acc[6], acc[7], FP16)));
+    }
+    __syncthreads();  // stage st is read by every thread: refill it
+    if (threadIdx.x == 0 && i + stages < steps) issue(i + stages);
+  }
+  if (tracer) {  // kind 4: the CTA's lifetime
+    uint64_t* r = trace + ((size_t)blockIdx.x * trace_cap + 1) * 4;
+    r[0] = (4ull << 56) | blockIdx.x;
+    r[1] = t0;
+    r[2] = globaltimer();
+    r[3] = 0;
+  }
+}
+
 // Generic slot reduction for the standalone ReduceScatter (any element
 // type): out[i] = sum_{s ascending} slot_s[i], accumulated in Acc.
 template <typename T, typename Acc>

@@ -556,6 +556,16 @@ int preload_kernels(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
   }
+  // the bulk-staged reduction's ring: up to 2 x 16 sources x 4 KB
+  for (const void* f : {reinterpret_cast<const void*>(rs_reduce_bulk_kernel<false>),
+                        reinterpret_cast<const void*>(rs_reduce_bulk_kernel<true>)}) {
+    cudaFuncAttributes a;
+    CUDA_TRY(cudaFuncGetAttributes(&a, f));
+    CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * SH_MAX_WORLD * kRbChunk + 256));
+    CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+  }
   return SH_OK;
 }
 
@@ -1771,12 +1781,30 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
     // timeline: per CTA (< trace grid) its counter wait (kind 3) and life (kind 4)
     uint64_t* tr = trace_slot(*rs, 2, s);
     const int tcap = tr ? rs->trace_cap : 0, tgrid = tr ? rs->trace_grid : 0;
-    if (dtype == SH_DTYPE_FP16)
+    if (env_int("SHB_RED_BULK", 1) && slot_elems % 8 == 0 && !rs->shares_gpu) {
+      // bulk-DMA staged form: W x 4 KB per step in a 3-deep (W > 8: 2-deep)
+      // shared-memory ring, two CTAs per SM at W <= 8 (one rank per GPU
+      // only: its full-size grid spinning on sibling ranks' counters would
+      // hold the SMs their GEMMs still need -- the forced-separate tests on
+      // one GPU timed out)
+      const int stages = W > 8 ? 2 : 3;
+      lc.dynamicSmemBytes = (size_t)stages * W * kRbChunk + 128 + 8 * stages;
+      lc.gridDim = dim3(sms * (W > 8 ? 1 : 2), 1, 1);
+      if (dtype == SH_DTYPE_FP16)
+        CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_bulk_kernel<true>, staging, o16, slot_elems,
+                                    W, stages, counters, target, rs->err_dev, w->timeout_ns, tr,
+                                    tcap, tgrid));
+      else
+        CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_bulk_kernel<false>, staging, o16, slot_elems,
+                                    W, stages, counters, target, rs->err_dev, w->timeout_ns, tr,
+                                    tcap, tgrid));
+    } else if (dtype == SH_DTYPE_FP16) {
       CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<true>, staging, o16, slot_elems, W,
                                   counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid));
-    else
+    } else {
       CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<false>, staging, o16, slot_elems, W,
                                   counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid));
+    }
   }
 
   return store_flags(s, fl, nfl, epoch);
