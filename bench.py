@@ -653,7 +653,9 @@ def measure_comm(sb, world, pe, N, rank, x, step, stream, barrier, max_over_rank
             barrier()
             ev = world.stop_trace()
         summ = timeline.exposed_comm(ev)
-        for kern in ("ag_gemm", "gemm_rs"):
+        # (rs_reduce: the separate reduction kernel of the RS on separate GPUs;
+        # every rank runs the same kernels, so the collectives below match)
+        for kern in ("ag_gemm", "gemm_rs", "rs_reduce"):
             rows_ = [s_ for s_ in summ if s_["kernel"] == kern]
             if rows_:
                 r_ = rows_[-1]
@@ -661,7 +663,8 @@ def measure_comm(sb, world, pe, N, rank, x, step, stream, barrier, max_over_rank
                              "exposed_wait_mean_us": max_over_ranks(r_["wait_mean_us"]),
                              "span_us": max_over_ranks(r_["span_us"] or 0.0)}
         out["exposed_how"] = ("device timeline of one traced step: per CTA, time spent waiting "
-                              "for a remote chunk (AG) / peers' rows (fused RS); max over ranks")
+                              "for a remote chunk (AG) / peers' rows (fused RS epilogue, or the "
+                              "separate reduction kernel rs_reduce); max over ranks")
     except Exception as e:  # noqa: BLE001
         out["exposed_error"] = f"{type(e).__name__}: {e}"[:300]
     return out
