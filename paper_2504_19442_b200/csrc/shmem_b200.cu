@@ -667,16 +667,16 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // every chunk in one raster region takes 292 us and the separate reduction
 // ~21 us, against 338 us for the GEMM whose own-chunk epilogues reduce --
 // those reductions compete with the last waves' operand streams and run at
-// a few warps per SM.  Ranks of one process that share a GPU keep the fused
-// form: a separate reduction kernel spinning on its peers' counters can take
-// the SMs a sibling rank's GEMM has not been granted yet (the persistent
-// grids are only co-resident if nothing else is queued between them).
+// a few warps per SM.  Ranks of one process that share a GPU run the same
+// form (their stream waits for the counters before the reduction launches,
+// so no reduction CTA can hold an SM a sibling's persistent GEMM needs).
 // Phased calls (serialising tools) are never fused.  SHB_RS_UNFUSED=1 / =0
-// forces either form (on shared GPUs too, for tests of the other form).
+// forces either form.
 bool rs_fused(int phase, int world, bool shares_gpu) {
+  (void)shares_gpu;
   if (phase != SH_PHASE_ALL) return false;
   if (const char* e = getenv("SHB_RS_UNFUSED")) return atoi(e) == 0;
-  return world == 1 || shares_gpu;
+  return world == 1;
 }
 
 }  // namespace
@@ -1759,6 +1759,15 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   int grid = (int)std::min<size_t>((nvec + 255) / 256, (size_t)sms * 4);
   if (grid < 1) grid = 1;
   const uint64_t* counters = sig_addr(w, *rs, rank, reduction_base);
+  if (rs->shares_gpu && rs_phase == SH_PHASE_ALL) {
+    // Ranks sharing a GPU (the separate form forced): the stream waits for
+    // every source's counter in the GPU front end before the reduction is
+    // launched, so no reduction CTA can occupy an SM that a sibling rank's
+    // persistent GEMM still needs (a forced-separate fuzz on one GPU
+    // deadlocked 40 % of its W >= 3 cases without this)
+    for (int q = 0; q < W; ++q)
+      if ((rc = stream_wait_geq(*rs, s, counters + q, target, w->timeout_ns))) return rc;
+  }
   // Programmatic dependent launch: the reduction's CTAs may start while the
   // GEMM still runs (it allows dependents right after its prologue) and
   // take SMs as its CTAs retire.  No griddepcontrol.wait: every byte the

@@ -39,7 +39,9 @@ def test_trace_of_a_tp_mlp_step(tmp_path):
     assert {"cta", "tile_epilogue", "chunk_wait"} <= kinds
     for r in range(W):
         mine = [e for e in events if e["rank"] == r]
-        assert {e["kernel"] for e in mine} == {"ag_gemm", "gemm_rs"}
+        # the RS's separate reduction kernel is a launch of its own
+        assert {e["kernel"] for e in mine} == {"ag_gemm", "gemm_rs", "rs_reduce"}
+        assert any(e["op"] == "peer_wait" for e in mine if e["kernel"] == "rs_reduce")
         # a chunk wait is only ever recorded for a remote chunk
         assert all(e["chunk"] != r for e in mine if e["op"] == "chunk_wait")
         for e in mine:
@@ -49,4 +51,4 @@ def test_trace_of_a_tp_mlp_step(tmp_path):
     assert doc and all(ev["ph"] == "X" for ev in doc)
     schemas.validate(doc, "trace", "trace")  # the reference's trace contract
     summary = exposed_comm(events)
-    assert len(summary) == 2 * W and all(s["span_us"] > 0 for s in summary)
+    assert len(summary) == 3 * W and all(s["span_us"] > 0 for s in summary)
