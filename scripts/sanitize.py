@@ -1,6 +1,9 @@
 """compute-sanitizer target: the fused ops at W=1 (the bench's own world) and
 W=2 on one GPU (the phased protocol the library picks under a
-kernel-serialising tool), small shapes, checked against the oracle.
+kernel-serialising tool), small shapes, checked against the oracle; and one
+rank of a W=4 world with the full GPU (tp_proxy.py, preset flags): the
+one-rank-per-GPU RS path (scattering GEMM with chunk-pair tiles, bulk-DMA
+reduction kernel), checked bit for bit.
 
     compute-sanitizer --tool memcheck|racecheck|synccheck python scripts/sanitize.py
 """
@@ -41,6 +44,25 @@ def run(W, m, n, k, calls=2):
         print(f"W={W} {m}x{n}x{k}: {calls} calls exact (phased={w.phased})", flush=True)
 
 
+def run_proxy():
+    import tp_proxy
+
+    px = tp_proxy.TpProxy(4, 512, 512, 512, 512, 512, timeout_s=60.0)
+    try:
+        for op in ("ag", "rs"):
+            px.time_op(op, "preset", 1, warmup=0)
+        torch.cuda.synchronize()
+        stag = px.world.heap_view(0, px.rsb.staging, torch.bfloat16, (px.W, px.rows, px.rs.n))
+        acc = torch.zeros(px.rows, px.rs.n, device=stag.device)
+        for s in range(px.W):
+            acc += stag[s].float()
+        assert torch.equal(px.y.view(torch.int16), acc.to(torch.bfloat16).view(torch.int16))
+        print("proxy W=4 rank 0 (separate GPUs path): RS bits exact", flush=True)
+    finally:
+        px.close()
+
+
 run(1, 512, 512, 256)
 run(2, 512, 256, 256)
+run_proxy()
 print("sanitize target ok")
