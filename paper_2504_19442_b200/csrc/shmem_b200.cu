@@ -264,6 +264,29 @@ void set_regions(TileParams& p, const int* starts, int nreg, int bm, int cluster
   p.reg_s0[nreg] = starts[nreg];
 }
 
+// Pair-chunk tiles (chunks of <= 128 rows, TileParams::pair_chunks): a CTA
+// pair's two CTAs take two consecutive chunk positions, one cluster per
+// tile.  Tile width 256 or 224, whichever needs less (waves x BN) of MMA
+// time per cluster: RS at TP=8, M=1024 (n=8192) is 128 tiles of 256 = 2
+// waves of 74 clusters at 86 % fill, or 148 tiles of 224 = 2 full waves
+// (TP=8 proxy, preset: 76.3 -> 73.4 us per call).  A stream-K split over
+// every cluster for the AG's partial wave (56 tiles on 74 clusters, 128
+// k-blocks) measured slower (73 -> 79 us) and is not offered.
+// SHB_PAIR_BN=256|224 forces the width.
+Cfg pair_chunk_cfg(int W, int n, int sms) {
+  const int clusters = sms / 2;
+  const int forced = env_int("SHB_PAIR_BN", 0);
+  auto make = [&](int bn) {
+    const int nblk = (n + bn - 1) / bn, tiles = (W / 2) * nblk;
+    return Cfg{bn, 2, std::min(tiles, clusters) * 2, 1, nblk, tiles};
+  };
+  if (forced == 224 || forced == 256) return make(forced);
+  const Cfg wide = make(256), narrow = make(224);
+  auto cost = [&](const Cfg& c) { return (double)((c.tiles + clusters - 1) / clusters) * c.bn; };
+  // narrow tiles stage more operand bytes per flop: 224 only for a clear gain
+  return cost(narrow) < 0.95 * cost(wide) ? narrow : wide;
+}
+
 Cfg choose_cfg(int rows, int world, int n, int sms, int share = 1, int k = 0) {
   // ranks sharing one GPU split its SMs, so that all their persistent GEMMs
   // are co-resident (their epilogues wait on each other's stores)
@@ -1413,8 +1436,7 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   if (pair_chunks) {
     int sms = num_sms(dev);
     if (rs->ranks_on_device > 1) sms = std::max(2, (sms / rs->ranks_on_device) & ~1);
-    const int nblk = (n + 255) / 256, tiles = (W / 2) * nblk;
-    cfg = Cfg{256, 2, std::min(tiles, sms / 2) * 2, 1, nblk, tiles};
+    cfg = pair_chunk_cfg(W, n, sms);
   }
   const bool own_by_ce = env_int("SHB_OWN_COPY_CE", 0) != 0;
   const bool do_comm = phase != SH_PHASE_COMPUTE;
@@ -1530,7 +1552,9 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
     if ((rc = zero_counter(rs->tile_counter, s))) return rc;
   }
   attach_wave(*rs, p);
-  p.dp_tiles = stream_k_split(cfg, (k + 63) / 64);
+  // pair tiles keep one cluster per tile (a stream-K split over every
+  // cluster measured slower on the TP=8 proxy, pair_chunk_cfg)
+  p.dp_tiles = pair_chunks ? cfg.tiles : stream_k_split(cfg, (k + 63) / 64);
   if (p.dp_tiles < p.num_tiles) {
     if ((rc = sk_reserve(rs->sk, cfg.grid / cfg.cg, cfg.cg, cfg.bn))) return rc;
     p.ws = rs->sk.ws;
@@ -1560,7 +1584,9 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
     int cnt = 0;
     for (int q = 0; q < W; ++q)
       if (q != rank) fl[cnt++] = sig_addr(w, *rs, q, done_base + rank);
-    if ((rc = store_flags(s, fl, cnt, epoch))) return rc;
+    // (SHB_DIAG_NOFLAGS: diagnostic only, what these stores cost a call on
+    // the TP proxy with preset flags)
+    if (!env_int("SHB_DIAG_NOFLAGS", 0) && (rc = store_flags(s, fl, cnt, epoch))) return rc;
   }
   if (use_comm) {
     CUDA_TRY(cudaEventRecord(rs->ev_done, rs->comm));
@@ -1626,8 +1652,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   if (pair_chunks) {
     int sms = num_sms(rs->device);
     if (rs->ranks_on_device > 1) sms = std::max(2, (sms / rs->ranks_on_device) & ~1);
-    const int nblk = (n + 255) / 256, tiles = (W / 2) * nblk;
-    cfg = Cfg{256, 2, std::min(tiles, sms / 2) * 2, 1, nblk, tiles};
+    cfg = pair_chunk_cfg(W, n, sms);
   }
   // With the reduction fused, the tiles of my own chunk wait for every peer's
   // rows; a cluster that reached them before finishing its peer-chunk tiles
@@ -1713,7 +1738,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   // last (rs_inter_order), or when nothing waits on peers.
   p.dp_tiles = p.num_tiles;
   {
-    const int dp = stream_k_split(cfg, (k + 63) / 64);
+    const int dp = pair_chunks ? cfg.tiles : stream_k_split(cfg, (k + 63) / 64);
     const int per_chunk = cfg.mblk * cfg.nblk;
     const bool safe = !fuse || W == 1 ||
                       (chunk_order[W - 1] == rank && p.num_tiles - dp <= per_chunk);
@@ -1816,7 +1841,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
     }
   }
 
-  return store_flags(s, fl, nfl, epoch);
+  return env_int("SHB_DIAG_NOFLAGS", 0) ? SH_OK : store_flags(s, fl, nfl, epoch);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,7 +1,7 @@
 """Device-timeline breakdown of the proxy kernels (preset flags): per CTA the
 MMA warp's waits for a free accumulator (epilogue-bound) and for operand
 stages (load-bound), epilogue windows by tile kind, CTA span.
-Usage: python scripts/proxy_trace.py W [ag|rs]"""
+Usage: python scripts/proxy_trace.py W [ag|rs]   (PROXY_M = per-job M, default 8192)"""
 import json
 import os
 import statistics
@@ -13,10 +13,11 @@ import tp_proxy  # noqa: E402
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 mode = os.environ.get("PROXY_MODE", "preset")
 ops = sys.argv[2:] or ["ag", "rs"]
+M = int(os.environ.get("PROXY_M", "8192"))
 if W == 1:
-    px = tp_proxy.TpProxy(1, 8192, 3584, 8192, 8192, 3584)
+    px = tp_proxy.TpProxy(1, M, 3584, 8192, 8192, 3584)
 else:
-    px = tp_proxy.TpProxy(W, 8192, 28672 // W, 8192, 8192, 28672 // W)
+    px = tp_proxy.TpProxy(W, M, 28672 // W, 8192, 8192, 28672 // W)
 out = {}
 try:
     for op in ops:
@@ -46,6 +47,9 @@ try:
                 d.setdefault("red", []).append(((e["t1_ns"] - e["t0_ns"]) / 1e3, e["drain_ns"] / 1e3))
             elif e["op"] == "cta":
                 d["end"] = e["t1_ns"] - t0
+                d["start"] = e["t0_ns"] - t0
+            if e["op"] == "mma_item":
+                d["first_mma"] = min(d.get("first_mma", 1 << 62), e["t0_ns"] - t0)
         lead = [d for d in per.values() if d["items"]]
         allepi = [x for d in per.values() for x in d["epi"]]
         allown = [x for d in per.values() for x in d["epi_own"]]
@@ -62,6 +66,10 @@ try:
             # tail: last accumulator ready (final MMA done) -> CTA end
             "tail_us": sorted(round((d["end"] - d.get("last_acc", d["end"])) / 1e3, 1)
                               for d in per.values() if "last_acc" in d)[::12],
+            # ramp: CTA start spread, first MMA work item start
+            "cta_start_us_max": max(d.get("start", 0) for d in per.values()) / 1e3,
+            "first_mma_us": sorted(round(d["first_mma"] / 1e3, 1) for d in lead if "first_mma" in d)[::12],
+            "end_us": sorted(round(d["end"] / 1e3, 1) for d in per.values())[::12],
             "last_acc_us_max": max(d.get("last_acc", 0) for d in per.values()) / 1e3,
             "peer_wait_us_max": max((e["t1_ns"] - e["t0_ns"]) / 1e3 for e in ev
                                     if e["op"] == "peer_wait") if any(e["op"] == "peer_wait" for e in ev) else 0,
