@@ -32,6 +32,49 @@ constexpr int kMaxWorld = 16;
 constexpr int MODE_AG = 0;
 constexpr int MODE_RS = 1;
 
+// Flags a kernel releases when its last CTA retires, in place of stream
+// memory operations after the launch.  Both users are write-after-read
+// flags -- AG done[rank] ("finished reading my gather buffer") and RS
+// producer[rank] ("finished reading my staging slots"): the peer overwrites
+// memory of THIS GPU once it sees them, so what must precede the flag are
+// reads served by this GPU's L2, all of them consumed (values used, bulk
+// loads completed on their mbarriers) before the CTA retires.  The last CTA
+// therefore orders them at gpu scope (acq_rel counting + fence) and stores
+// the flags relaxed at system scope; a system-scope release would also wait
+// for every earlier write of the kernel to become visible system-wide.
+// TP=8 proxy, M=1024, preset flags, per call: AG 73.0 us with the 7 stream
+// memory ops (~2.8 us each in the GPU front end), 60.4 with st.release.sys
+// here (or a one-warp store kernel after the GEMM), 53.8 with this form =
+// the call without any flag store (profiles/r2_exit_release/).
+// SHB_EXIT_SYS_RELEASE=1 selects the system-scope release stores.
+struct ExitRelease {
+  uint64_t* ptr[kMaxWorld];
+  uint64_t value;
+  unsigned int* ctr;  // CTAs retired so far; the last one resets it to 0
+  int count;          // 0: nothing to release
+  int sys_release;    // 1: st.release.sys (see above)
+};
+
+// One thread per CTA, after a CTA-wide barrier that follows every read the
+// flags vouch for.  The counter reset is ordered before the next launch on
+// the stream (the GEMM's main body starts after griddepcontrol.wait, the
+// reduction after its GEMM's prologue).
+__device__ __forceinline__ void exit_release(const ExitRelease& r) {
+  if (r.count <= 0) return;
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(r.ctr) : "memory");
+  if (old + 1 == gridDim.x) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(r.ctr) : "memory");
+    for (int i = 0; i < r.count; ++i) {
+      if (r.sys_release)
+        st_release_sys(r.ptr[i], r.value);
+      else
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(r.ptr[i]), "l"(r.value) : "memory");
+    }
+  }
+}
+
 struct TileParams {
   int rows;       // rows per chunk (m / world)
   int n, k;
@@ -99,6 +142,7 @@ struct TileParams {
   float* ws;                          // clusters x (CG*128) x BN fp32 partials
   uint64_t* ws_flags;                 // clusters x CG x 4 epilogue warps
   uint64_t ws_epoch;                  // launch counter of this workspace
+  ExitRelease rel;                    // AG: done[rank] on every peer; fused RS: producer[rank]
   // Wave lockstep: cluster c runs data-parallel tiles c, c+C, c+2C, ...; the
   // i-th of them forms wave i.  When K is long, the operand reuse between the
   // tiles of a wave comes only from their walking K together (a block's
@@ -1109,6 +1153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
   }
+  if (threadIdx.x == 0) exit_release(p.rel);
 }
 
 // ---------------------------------------------------------------------------
@@ -1128,7 +1173,8 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
                                                         const uint64_t* counters, uint64_t target,
                                                         int* err, uint64_t timeout_ns,
                                                         uint64_t* trace, int trace_cap,
-                                                        int trace_grid) {
+                                                        int trace_grid,
+                                                        const __grid_constant__ ExitRelease rel) {
   constexpr int kGroup = 8;
   const bool tracer = trace != nullptr && threadIdx.x == 0 && (int)blockIdx.x < trace_grid &&
                       trace_cap >= 2;
@@ -1192,6 +1238,11 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(const uint16_t* __restri
     r[2] = globaltimer();
     r[3] = 0;
   }
+  // producer[rank] on every peer: this rank has read its staging slots
+  if (rel.count > 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) exit_release(rel);
+  }
 }
 
 // The same reduction with the W source slots staged by bulk copies (the DMA
@@ -1205,7 +1256,7 @@ template <bool FP16>
 __global__ void __launch_bounds__(256) rs_reduce_bulk_kernel(
     const uint16_t* __restrict__ staging, uint16_t* __restrict__ out, size_t slot_elems, int world,
     int stages, const uint64_t* counters, uint64_t target, int* err, uint64_t timeout_ns,
-    uint64_t* trace, int trace_cap, int trace_grid) {
+    uint64_t* trace, int trace_cap, int trace_grid, const __grid_constant__ ExitRelease rel) {
   extern __shared__ uint8_t rb_raw[];
   uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rb_raw) + 127) &
                                             ~uintptr_t(127));
@@ -1276,6 +1327,11 @@ __global__ void __launch_bounds__(256) rs_reduce_bulk_kernel(
     r[1] = t0;
     r[2] = globaltimer();
     r[3] = 0;
+  }
+  // producer[rank] on every peer: this rank has read its staging slots
+  if (rel.count > 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) exit_release(rel);
   }
 }
 

@@ -722,6 +722,7 @@ struct RankState {
   int ranks_on_device = 1;  // ranks of this process on `device` (incl. this one)
   SkWorkspace sk;           // stream-K partials of this rank's AG launches
   int* tile_counter = nullptr;  // dynamic tile scheduler counter (zeroed per launch)
+  unsigned int* exit_ctr = nullptr;  // retired-CTA counts (ExitRelease): AG, RS GEMM, reduction
   uint64_t* wave = nullptr;     // per-cluster wave progress flags (epoch-tagged)
   uint64_t wave_epoch = 0;
   uint64_t* trace = nullptr;  // [max_launches][grid_max][cap][4] timeline records
@@ -755,6 +756,8 @@ int init_rank_common(sh_world* w, RankState& rs) {
   if ((rc = sk_reserve(rs.sk, num_sms(rs.device) / 2, 2, 512))) return rc;
   CUDA_TRY(cudaMalloc(&rs.tile_counter, 256));
   CUDA_TRY(cudaMemset(rs.tile_counter, 0, 256));
+  CUDA_TRY(cudaMalloc(&rs.exit_ctr, 4 * sizeof(unsigned int)));
+  CUDA_TRY(cudaMemset(rs.exit_ctr, 0, 4 * sizeof(unsigned int)));
   CUDA_TRY(cudaMalloc(&rs.wave, kWaveFlags * sizeof(uint64_t)));
   CUDA_TRY(cudaMemset(rs.wave, 0, kWaveFlags * sizeof(uint64_t)));
   CUDA_TRY(cudaStreamCreateWithFlags(&rs.comm, cudaStreamNonBlocking));
@@ -831,6 +834,23 @@ int store_flags(cudaStream_t s, uint64_t* const* ptrs, int count, uint64_t value
   flag_store_list_kernel<<<1, 32, 0, s>>>(l, nk, value);
   CUDA_TRY(cudaGetLastError());
   return SH_OK;
+}
+
+// Flags released by the last retiring CTA of the kernel that does the
+// reads they vouch for (ExitRelease) instead of stream memory operations
+// after it.  SHB_EXIT_RELEASE=0: the stream operations (store_flags).
+bool exit_release_on() { return env_int("SHB_EXIT_RELEASE", 1) != 0; }
+
+ExitRelease make_release(uint64_t* const* ptrs, int count, uint64_t value, unsigned int* ctr) {
+  ExitRelease r;
+  memset(&r, 0, sizeof(r));
+  if (env_int("SHB_DIAG_NOFLAGS", 0)) return r;  // diagnostic (see the AG tail)
+  for (int i = 0; i < count; ++i) r.ptr[i] = ptrs[i];
+  r.count = count;
+  r.value = value;
+  r.ctr = ctr;
+  r.sys_release = env_int("SHB_EXIT_SYS_RELEASE", 0) != 0 ? 1 : 0;
+  return r;
 }
 
 // Copies of the push / put / get paths.  Across devices (peer access over
@@ -1006,6 +1026,7 @@ int sh_world_destroy(sh_world* w) {
     if (rs.err_host) cudaFreeHost(rs.err_host);
     if (rs.trace) cudaFree(rs.trace);
     if (rs.tile_counter) cudaFree(rs.tile_counter);
+    if (rs.exit_ctr) cudaFree(rs.exit_ctr);
     if (rs.wave) cudaFree(rs.wave);
     if (rs.sk.ws) cudaFree(rs.sk.ws);
     if (rs.sk.flags) cudaFree(rs.sk.flags);
@@ -1574,20 +1595,23 @@ int sh_ag_gemm_ex(sh_world* w, int rank, const void* a_shard, const void* b, voi
   }
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
+  // ---- publish "finished reading my gather buffer" to every peer: done[rank]
+  // on each, released by the GEMM's last retiring CTA (or stream operations
+  // after it); then join the comm stream so the call completes only when
+  // a_shard is free.
+  uint64_t* fl[SH_MAX_WORLD];
+  int cnt = 0;
+  for (int q = 0; q < W; ++q)
+    if (q != rank) fl[cnt++] = sig_addr(w, *rs, q, done_base + rank);
+  const bool in_kernel = exit_release_on();
+  if (in_kernel) p.rel = make_release(fl, cnt, epoch, rs->exit_ctr + 0);
   if ((rc = launch_gemm<MODE_AG>(dtype, cfg, maps, p, s, rs->shares_gpu || phase != SH_PHASE_ALL)))
     return rc;
-
-  // ---- publish "finished reading my gather buffer" to every peer, then
-  // join the comm stream so the call completes only when a_shard is free.
-  if (W > 1) {
-    uint64_t* fl[SH_MAX_WORLD];
-    int cnt = 0;
-    for (int q = 0; q < W; ++q)
-      if (q != rank) fl[cnt++] = sig_addr(w, *rs, q, done_base + rank);
-    // (SHB_DIAG_NOFLAGS: diagnostic only, what these stores cost a call on
-    // the TP proxy with preset flags)
-    if (!env_int("SHB_DIAG_NOFLAGS", 0) && (rc = store_flags(s, fl, cnt, epoch))) return rc;
-  }
+  // (SHB_DIAG_NOFLAGS: diagnostic only, what these stores cost a call on the
+  // TP proxy with preset flags)
+  if (!in_kernel && cnt > 0 && !env_int("SHB_DIAG_NOFLAGS", 0) &&
+      (rc = store_flags(s, fl, cnt, epoch)))
+    return rc;
   if (use_comm) {
     CUDA_TRY(cudaEventRecord(rs->ev_done, rs->comm));
     CUDA_TRY(cudaStreamWaitEvent(s, rs->ev_done, 0));
@@ -1763,22 +1787,28 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   p.fuse_reduce = fuse ? 1 : 0;
   p.err = rs->err_dev;
   p.timeout_ns = w->timeout_ns;
-  if (rs_phase != SH_PHASE_COMPUTE &&
-      (rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s, rs->shares_gpu || rs_phase != SH_PHASE_ALL)))
-    return rc;
-  if (rs_phase == SH_PHASE_COMM) return SH_OK;  // scatter only: reduce in a later phase call
-
   // reduction of my W staging slots in ascending source order: fused into the
   // epilogue of my own chunk's tiles (scheduled last, rs_inter_order), or a
-  // separate vectorised pass when SHB_RS_UNFUSED=1
-  // publish "reduced epoch" to every peer: frees my staging slots for their
-  // next call (the join of collectives.py:1-10, made a flag).  My own slot is
-  // rewritten only by my own next call, stream-ordered, so no self flag.
+  // separate vectorised pass.  Then publish "reduced epoch" to every peer:
+  // frees my staging slots for their next call (the join of
+  // collectives.py:1-10, made a flag), released by the last retiring CTA of
+  // the kernel that reads the slots (or stream operations after it).  My own
+  // slot is rewritten only by my own next call, stream-ordered, so no self flag.
   uint64_t* fl[SH_MAX_WORLD];
   int nfl = 0;
   for (int q = 0; q < W; ++q)
     if (q != rank) fl[nfl++] = sig_addr(w, *rs, q, producer_base + rank);
-  if (fuse) return store_flags(s, fl, nfl, epoch);
+  const bool in_kernel = exit_release_on();
+  if (fuse && in_kernel) p.rel = make_release(fl, nfl, epoch, rs->exit_ctr + 1);
+  if (rs_phase != SH_PHASE_COMPUTE &&
+      (rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s, rs->shares_gpu || rs_phase != SH_PHASE_ALL)))
+    return rc;
+  if (rs_phase == SH_PHASE_COMM) return SH_OK;  // scatter only: reduce in a later phase call
+  const bool host_flags = !in_kernel && nfl > 0 && !env_int("SHB_DIAG_NOFLAGS", 0);
+  if (fuse) return host_flags ? store_flags(s, fl, nfl, epoch) : SH_OK;
+  ExitRelease rel;
+  memset(&rel, 0, sizeof(rel));
+  if (in_kernel) rel = make_release(fl, nfl, epoch, rs->exit_ctr + 2);
   int sms = num_sms(rs->device);
   size_t nvec = (slot_elems + 7) / 8;
   int grid = (int)std::min<size_t>((nvec + 255) / 256, (size_t)sms * 4);
@@ -1827,21 +1857,23 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
       if (dtype == SH_DTYPE_FP16)
         CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_bulk_kernel<true>, staging, o16, slot_elems,
                                     W, stages, counters, target, rs->err_dev, w->timeout_ns, tr,
-                                    tcap, tgrid));
+                                    tcap, tgrid, rel));
       else
         CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_bulk_kernel<false>, staging, o16, slot_elems,
                                     W, stages, counters, target, rs->err_dev, w->timeout_ns, tr,
-                                    tcap, tgrid));
+                                    tcap, tgrid, rel));
     } else if (dtype == SH_DTYPE_FP16) {
       CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<true>, staging, o16, slot_elems, W,
-                                  counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid));
+                                  counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid,
+                                  rel));
     } else {
       CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_kernel<false>, staging, o16, slot_elems, W,
-                                  counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid));
+                                  counters, target, rs->err_dev, w->timeout_ns, tr, tcap, tgrid,
+                                  rel));
     }
   }
 
-  return env_int("SHB_DIAG_NOFLAGS", 0) ? SH_OK : store_flags(s, fl, nfl, epoch);
+  return host_flags ? store_flags(s, fl, nfl, epoch) : SH_OK;
 }
 
 // ---------------------------------------------------------------------------

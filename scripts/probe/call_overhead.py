@@ -13,8 +13,10 @@ W = int(os.environ.get("PROXY_W", "8"))
 M = int(os.environ.get("PROXY_M", "1024"))
 px = tp_proxy.TpProxy(W, M, 28672 // W, 8192, 8192, 28672 // W)
 out = {}
-knobs = {"base": {}, "flag_kernel": {"SHB_FLAG_KERNEL": "1"}, "no_flags": {"SHB_DIAG_NOFLAGS": "1"},
-         "red_nopdl": {"SHB_RED_PDL": "0"}, "nopdl": {"SHB_PDL": "0"}}
+knobs = {"base": {}, "sys_release": {"SHB_EXIT_SYS_RELEASE": "1"},
+         "memops": {"SHB_EXIT_RELEASE": "0"},
+         "flag_kernel": {"SHB_EXIT_RELEASE": "0", "SHB_FLAG_KERNEL": "1"},
+         "no_flags": {"SHB_DIAG_NOFLAGS": "1"}}
 try:
     evs = []
     for _ in range(30):
