@@ -174,12 +174,19 @@ def test_ag_gemm_wait_counts_and_no_barriers(rng):
         shards = [ints(rng, -2, 3, (128, 64)) for _ in range(4)]
         b = ints(rng, -1, 2, (64, 64))
         w.reset_counters()
+        w.start_trace(records_per_cta=64, launches=2)
         run_np(w, lambda pe: ag_gemm(pe, dev(shards[pe.rank], pe), dev(b, pe), shape,
                                  ag_order_switch(pe.rank, 4), bufs))
+        events = w.stop_trace()
         for r in range(4):
             c = w.counters(r)
             assert c.get("wait", 0) == 3
             assert c.get("barrier_all", 0) == 0
+            # the device side of those waits (not the host wrapper's count):
+            # the producers' acquire spins on ready[c] (timeline kind 1) cover
+            # exactly the 3 remote chunks, never the rank's own shard
+            waited = {e["chunk"] for e in events if e["rank"] == r and e["op"] == "chunk_wait"}
+            assert waited == set(range(4)) - {r}
 
 
 def test_ag_gemm_shape_mismatch():
