@@ -88,6 +88,8 @@ int sh_fill_signals(sh_world* w, int rank, int base, int count, uint64_t value, 
 /* Device-side timeouts (bounded spins) land in a host-mapped error word per
  * rank; nonzero => SynchronizationFault (reference sched.py:227-238). */
 int sh_poll_error(sh_world* w, int rank, int* code);
+/* Clears the error word and the kernels' retired-CTA counters (the last-CTA
+ * flag release); call with the rank's device drained (World.recover). */
 int sh_clear_error(sh_world* w, int rank);
 
 /* Fused AllGather+GEMM for rank `rank`: replaces pipelines.ag_gemm

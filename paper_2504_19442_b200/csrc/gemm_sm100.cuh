@@ -101,6 +101,8 @@ struct TileParams {
   int ag_sub;                         // AG: row ranges per pushed shard (ready counts them)
   int ag_sub_rows;                    // AG: rows per range (multiple of 256)
   uint64_t* rs_count[kMaxWorld];      // RS: &pad_d[reduction + rank]
+  uint32_t rs_gpu_scope;              // RS: bit d -> chunk d's counter released at gpu scope
+                                      // (my own chunk: staging and its reducer are on this GPU)
   const uint64_t* rs_free;            // RS: my pad, producer[d] >= epoch-1: d reduced last call
   const uint64_t* rs_mine;            // RS: my pad, reduction[s] (elements delivered by s)
   uint64_t rs_target;                 // RS: epoch * rows * n, a chunk fully delivered
@@ -157,6 +159,15 @@ struct TileParams {
   int* err;                           // host-mapped error word
   uint64_t timeout_ns;
 };
+
+// RS: publish `cnt` more elements of chunk d delivered (data before count:
+// the caller completed the tile's bulk stores and fenced the async proxy)
+__device__ __forceinline__ void rs_publish(const TileParams& p, int d, uint64_t cnt) {
+  if ((p.rs_gpu_scope >> d) & 1u)
+    red_add_release_gpu(p.rs_count[d], cnt);
+  else
+    red_add_release_sys(p.rs_count[d], cnt);
+}
 
 __device__ __forceinline__ void trace_rec(const TileParams& p, int slot, uint64_t kind_aux,
                                           uint64_t t0, uint64_t t1, uint64_t tile) {
@@ -915,7 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // publish before waiting on the peers: they may be waiting on it
         bulk_wait<0>();
         fence_proxy_async_global();
-        red_add_release_sys(p.rs_count[pend_chunk], pend_count);
+        rs_publish(p, pend_chunk, pend_count);
         pend_chunk = -1;
       }
       if (fused_own && !peers_in) {
@@ -1094,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (pend_chunk >= 0) {
             bulk_wait<C::NSUB>();
             fence_proxy_async_global();
-            red_add_release_sys(p.rs_count[pend_chunk], pend_count);
+            rs_publish(p, pend_chunk, pend_count);
           }
           pend_chunk = -1;
           // count the elements this warp actually delivered (TMA clips the
@@ -1120,7 +1131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       bulk_wait<0>();
       if (MODE == MODE_RS && pend_chunk >= 0) {
         fence_proxy_async_global();
-        red_add_release_sys(p.rs_count[pend_chunk], pend_count);
+        rs_publish(p, pend_chunk, pend_count);
       }
     }
     __syncwarp();

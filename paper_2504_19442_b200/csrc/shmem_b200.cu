@@ -1134,6 +1134,12 @@ int sh_clear_error(sh_world* w, int rank) {
   RankState* rs = rank_of(w, rank);
   if (!rs) return fail(SH_ERR_ARG, "bad rank %d", rank);
   *reinterpret_cast<volatile int*>(rs->err_host) = 0;
+  // a kernel that bailed out on a timeout may have left a retired-CTA count
+  // behind (ExitRelease); the caller has drained the device (World.recover)
+  if (rs->exit_ctr) {
+    CUDA_TRY(cudaSetDevice(rs->device));
+    CUDA_TRY(cudaMemset(rs->exit_ctr, 0, 4 * sizeof(unsigned int)));
+  }
   return SH_OK;
 }
 
@@ -1749,6 +1755,12 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   for (int i = 0; i < W; ++i) p.order[i] = chunk_order[i];
   p.epoch = epoch;
   for (int d = 0; d < W; ++d) p.rs_count[d] = sig_addr(w, *rs, d, reduction_base + rank);
+  // my own chunk's staging slot and its reducer (the separate kernel or the
+  // fused epilogue) are on this GPU: gpu-scope release for its counter.
+  // SHB_RS_OWN_GPU=0: system scope; SHB_DIAG_RS_GPU_SCOPE=1: every chunk at
+  // gpu scope (diagnostic, valid only when every rank shares this GPU).
+  p.rs_gpu_scope = env_int("SHB_RS_OWN_GPU", 1) ? (1u << rank) : 0u;
+  if (env_int("SHB_DIAG_RS_GPU_SCOPE", 0)) p.rs_gpu_scope = ~0u;
   p.rs_free = sig_addr(w, *rs, rank, producer_base);
   const uint16_t* staging =
       reinterpret_cast<const uint16_t*>(static_cast<char*>(rs->peer[rank]) + staging_off);
@@ -1800,6 +1812,10 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
     if (q != rank) fl[nfl++] = sig_addr(w, *rs, q, producer_base + rank);
   const bool in_kernel = exit_release_on();
   if (fuse && in_kernel) p.rel = make_release(fl, nfl, epoch, rs->exit_ctr + 1);
+  // the separate reduction's timeline slot is cleared (a memset on the
+  // stream) before the GEMM, so a traced call keeps the programmatic
+  // dependent launch between the two kernels
+  uint64_t* red_tr = (!fuse && rs_phase != SH_PHASE_COMM) ? trace_slot(*rs, 2, s) : nullptr;
   if (rs_phase != SH_PHASE_COMPUTE &&
       (rc = launch_gemm<MODE_RS>(dtype, cfg, maps, p, s, rs->shares_gpu || rs_phase != SH_PHASE_ALL)))
     return rc;
@@ -1843,7 +1859,7 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
     lc.numAttrs = red_pdl ? 1 : 0;
     uint16_t* o16 = static_cast<uint16_t*>(out);
     // timeline: per CTA (< trace grid) its counter wait (kind 3) and life (kind 4)
-    uint64_t* tr = trace_slot(*rs, 2, s);
+    uint64_t* tr = red_tr;
     const int tcap = tr ? rs->trace_cap : 0, tgrid = tr ? rs->trace_grid : 0;
     if (env_int("SHB_RED_BULK", 1) && slot_elems % 8 == 0 && !rs->shares_gpu) {
       // bulk-DMA staged form: W x 4 KB per step in a 3-deep (W > 8: 2-deep)
