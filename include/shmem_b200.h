@@ -99,7 +99,9 @@ int sh_clear_error(sh_world* w, int rank);
  *   gathered_off : offset of the symmetric (W*m/W*k) gather buffer
  *   ready_base   : W signals; ready[src] counts src's landed row ranges:
  *                  (epoch-1)*S + j once range j of S landed (S = sh_ag_subchunks)
- *   done_base    : W signals; done[p] = epoch once rank p finished the call
+ *   done_base    : W signals; done[p] = epoch once rank p finished reading its
+ *                  gather buffer (stored into every peer by the GEMM's last
+ *                  retiring CTA; SHB_EXIT_RELEASE=0: stream writes after it)
  *   chunk_order  : W ints, a permutation (first-visit order of the TileSchedule)
  *   epoch        : monotone call counter (>= 1), identical on every rank */
 int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* c,
@@ -111,6 +113,7 @@ int sh_ag_gemm(sh_world* w, int rank, const void* a_shard, const void* b, void* 
  *   a : (m, k)   b : (k, n)   out : (m/W, n) = row block `rank` of sum_r a_r @ b_r
  *   staging_off   : offset of the symmetric W*(m/W)*n staging buffer
  *   producer_base : W signals; producer[d] = epoch once rank d reduced this call
+ *                   (stored by the last retiring CTA of the reducing kernel)
  *   reduction_base: W signals; reduction[s] counts elements delivered by s */
 int sh_gemm_rs(sh_world* w, int rank, const void* a, const void* b, void* out,
                size_t staging_off, int producer_base, int reduction_base, int m, int n, int k,
