@@ -579,13 +579,13 @@ int preload_kernels(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
   }
-  // the bulk-staged reduction's ring: up to 2 x 16 sources x 4 KB
+  // the bulk-staged reduction's ring: stages x sources x 4 KB, up to 220 KB
   for (const void* f : {reinterpret_cast<const void*>(rs_reduce_bulk_kernel<false>),
                         reinterpret_cast<const void*>(rs_reduce_bulk_kernel<true>)}) {
     cudaFuncAttributes a;
     CUDA_TRY(cudaFuncGetAttributes(&a, f));
     CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  2 * SH_MAX_WORLD * kRbChunk + 256));
+                                  220 * 1024 + 256));
     CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
   }
@@ -1867,9 +1867,16 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
       // only: its full-size grid spinning on sibling ranks' counters would
       // hold the SMs their GEMMs still need -- the forced-separate tests on
       // one GPU timed out)
-      const int stages = W > 8 ? 2 : 3;
+      // SHB_RB_CTAS (CTAs per SM) / SHB_RB_STAGES: A/B knobs, clamped to the
+      // shared memory per SM.  TP=8 proxy RS (C4, preset, medians of 4 x 20
+      // calls): 2 x 3 stages 342.1 us, 1 x 6 347.9, 1 x 4 356.6, 2 x 2 355.0
+      // (scripts/probe/rb_stages.sh)
+      const int per_sm = std::max(1, std::min(2, env_int("SHB_RB_CTAS", W > 8 ? 1 : 2)));
+      int stages = env_int("SHB_RB_STAGES", W > 8 ? 2 : 3);
+      const int max_st = (int)((220 * 1024 / per_sm) / ((size_t)W * kRbChunk));
+      stages = std::max(1, std::min(stages, std::max(1, max_st)));
       lc.dynamicSmemBytes = (size_t)stages * W * kRbChunk + 128 + 8 * stages;
-      lc.gridDim = dim3(sms * (W > 8 ? 1 : 2), 1, 1);
+      lc.gridDim = dim3(sms * per_sm, 1, 1);
       if (dtype == SH_DTYPE_FP16)
         CUDA_TRY(cudaLaunchKernelEx(&lc, rs_reduce_bulk_kernel<true>, staging, o16, slot_elems,
                                     W, stages, counters, target, rs->err_dev, w->timeout_ns, tr,
