@@ -1285,6 +1285,10 @@ int sh_query_tile_config(int rows, int world, int n, int* bn, int* cta_group, in
   int dev = 0;
   cudaGetDevice(&dev);
   Cfg c = choose_cfg(rows, world, n, num_sms(dev));
+  // chunks of <= 128 rows in an even world: both ops launch pair-chunk tiles
+  // (the RS unless its reduction is forced into the GEMM, SHB_RS_UNFUSED=0)
+  if (world % 2 == 0 && rows <= 128 && c.cg == 1 && !g_force_bn && !g_force_cg)
+    c = pair_chunk_cfg(world, n, num_sms(dev));
   if (bn) *bn = c.bn;
   if (cta_group) *cta_group = c.cg;
   if (grid) *grid = c.grid;

@@ -154,7 +154,7 @@ def test_world_refuses_without_cuda():
         init_world(WorldSpec(world_size=1))
 
 
-def test_tile_choice_small_chunks_use_single_cta_tiles():
+def test_tile_choice_small_chunks():
     # host-side tile choice (no GPU needed: 148 SMs assumed): TP=8 at M=1024
     # gives 128-row chunks, where a 256-row pair tile would be half padding
     lib = _lib.load()
@@ -165,8 +165,11 @@ def test_tile_choice_small_chunks_use_single_cta_tiles():
                                         ctypes.byref(grid)) == _lib.SH_OK
         return bn.value, cg.value, grid.value
 
-    assert query(128, 8, 3584) == (256, 1, 112)   # AG C5 M=1024 TP=8: one wave of 1-CTA tiles
-    assert query(128, 8, 8192)[1] == 1            # RS C5 M=1024 TP=8
+    # C5 M=1024 TP=8: 128-row chunks; a CTA pair takes two chunk positions,
+    # 224 columns wide when that fills the waves better (pair_chunk_cfg)
+    assert query(128, 8, 3584) == (224, 2, 128)   # AG: 64 tiles, one wave
+    assert query(128, 8, 8192) == (224, 2, 148)   # RS: 148 tiles = 2 full waves
+    assert query(128, 7, 3584)[1] == 1            # odd world: single-CTA tiles
     assert query(1024, 8, 3584)[:2] == (256, 2)   # C3: pair tiles
     assert query(8192, 1, 3584) == (256, 2, 148)
     assert query(512, 4, 7168)[1] == 2
