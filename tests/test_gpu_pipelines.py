@@ -792,3 +792,39 @@ def test_pair_chunk_tiles_exact(rng, monkeypatch, world_size, rows, n, k, unfuse
             assert np.array_equal(staging, oracle.staging_layout(amats, [b] * world_size, r))
             gathered = to_np(w.read_tensor(r, agb.gathered, BF16, (m, k)))
             assert np.array_equal(gathered, oracle.gathered_layout(shards))
+
+
+@pytest.mark.parametrize("exit_release", ["1", "0"])
+def test_war_flags_hold_the_epoch_after_each_call(rng, monkeypatch, exit_release):
+    # the write-after-read flags: done[p] (AG, "p finished reading its gather
+    # buffer") and producer[d] (RS, "d reduced its staging slots") hold the
+    # call's epoch on every peer after each call -- stored by the last
+    # retiring CTA of the reading kernel (default) or by stream writes after
+    # it (SHB_EXIT_RELEASE=0); the products stay bit-exact on every call
+    monkeypatch.setenv("SHB_EXIT_RELEASE", exit_release)
+    W, rows, n, k = 4, 256, 256, 512
+    m = rows * W
+    shape = ProblemShape(m=m, n=n, k=k, dtype="bfloat16")
+    with make_world(W, heap_bytes=1 << 25) as w:
+        agb, rsb = make_ag_gemm_buffers(w, shape), make_gemm_rs_buffers(w, shape)
+        for epoch in (1, 2, 3):
+            shards = [ints(rng, -2, 3, (rows, k)) for _ in range(W)]
+            amats = [ints(rng, -1, 2, (m, k)) for _ in range(W)]
+            b = ints(rng, -1, 2, (k, n))
+
+            def body(pe):
+                x, a, bb = dev(shards[pe.rank], pe), dev(amats[pe.rank], pe), dev(b, pe)
+                h = ag_gemm(pe, x, bb, shape, ag_order_switch(pe.rank, W), agb, reset=False)
+                y = gemm_rs(pe, a, bb, shape, rs_inter_order(pe.ctx, 1, W), rsb, reset=False)
+                return h, y
+
+            outs = run_np(w, body)
+            rs_ref = oracle.gemm_rs_reference(amats, [b] * W)
+            for r, (h, y) in enumerate(outs):
+                assert np.array_equal(h, oracle.ag_gemm_reference(shards, b))
+                assert np.array_equal(y, rs_ref[r])
+            for r in range(W):
+                for p in range(W):
+                    if p != r:
+                        assert w.sig_read(r, agb.done.base + p) == epoch
+                        assert w.sig_read(r, rsb.producer.base + p) == epoch
