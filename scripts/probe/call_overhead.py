@@ -13,8 +13,10 @@ W = int(os.environ.get("PROXY_W", "8"))
 M = int(os.environ.get("PROXY_M", "1024"))
 px = tp_proxy.TpProxy(W, M, 28672 // W, 8192, 8192, 28672 // W)
 out = {}
-knobs = {"base": {}, "own_sys": {"SHB_RS_OWN_GPU": "0"}, "all_gpu": {"SHB_DIAG_RS_GPU_SCOPE": "1"},
-         "memops": {"SHB_EXIT_RELEASE": "0"}, "no_flags": {"SHB_DIAG_NOFLAGS": "1"}}
+knobs = {"base": {}, "sys_release": {"SHB_EXIT_SYS_RELEASE": "1"},
+         "memops": {"SHB_EXIT_RELEASE": "0"},
+         "flag_kernel": {"SHB_EXIT_RELEASE": "0", "SHB_FLAG_KERNEL": "1"},
+         "no_flags": {"SHB_DIAG_NOFLAGS": "1"}, "all_gpu": {"SHB_DIAG_RS_GPU_SCOPE": "1"}}
 try:
     evs = []
     for _ in range(30):
