@@ -1764,7 +1764,11 @@ int sh_gemm_rs_ex(sh_world* w, int rank, const void* a, const void* b, void* out
   // SHB_RS_OWN_GPU=0: system scope; SHB_DIAG_RS_GPU_SCOPE=1: every chunk at
   // gpu scope (diagnostic, valid only when every rank shares this GPU).
   p.rs_gpu_scope = env_int("SHB_RS_OWN_GPU", 1) ? (1u << rank) : 0u;
-  if (env_int("SHB_DIAG_RS_GPU_SCOPE", 0)) p.rs_gpu_scope = ~0u;
+  if (env_int("SHB_DIAG_RS_GPU_SCOPE", 0)) {
+    bool all_here = true;  // honoured only when every rank's staging is on this GPU
+    for (int q = 0; q < W; ++q) all_here = all_here && w->r[q].device == rs->device;
+    if (all_here) p.rs_gpu_scope = ~0u;
+  }
   p.rs_free = sig_addr(w, *rs, rank, producer_base);
   const uint16_t* staging =
       reinterpret_cast<const uint16_t*>(static_cast<char*>(rs->peer[rank]) + staging_off);
